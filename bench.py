@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""BOBA reorder + COO->CSR throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c5|c4] [--impl ours|reference]
+
+A step = one pass of the hot path over the whole synthetic graph, inputs
+already resident in HBM: first occurrence -> rank compaction -> relabel ->
+COO->CSR (reference bench.py:135-149: reorder_ms + convert_ms).  Metric:
+GEdges/s = m / step time, whole job (sum over ranks).  The JSON line also
+carries the per-phase roofline against MEASURED_PEAKS.json, the end-to-end
+number through the host-buffer C-ABI entry (H2D + pipeline + D2H), the SpMV
+e2e speedup of BOBA vs the randomly labelled CSR, and the CPU oracle timed
+on this host.  ``--impl reference`` times the reference algorithm's CPU
+restatement (oracle/, the reference is pure Python/numba and has no compiled
+form to build) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (kind, params, human description)
+    "c1": ("rmat", dict(scale=16, ef=8), "R-MAT scale 16 edge factor 8"),
+    "c2": ("rmat", dict(scale=22, ef=16), "R-MAT scale 22 edge factor 16"),
+    "c3": ("grid", dict(rows=4096, cols=4096), "2D grid 4096x4096"),
+    "c5": ("rmat", dict(scale=24, ef=16), "R-MAT scale 24 edge factor 16"),
+    "c4": ("rmat", dict(scale=26, ef=16), "R-MAT scale 26 edge factor 16"),
+}
+GEN_SEED, LABEL_SEED = 1, 7
+SPMV_ITERS = {"c1": 10, "c2": 10, "c3": 100, "c5": 10, "c4": 10}
+
+
+def graph_size(cfg):
+    kind, p, _ = CONFIGS[cfg]
+    if kind == "rmat":
+        return 1 << p["scale"], p["ef"] << p["scale"]
+    r, c = p["rows"], p["cols"]
+    return r * c, 2 * r * (c - 1) + 2 * (r - 1) * c
+
+
+def alg_bytes(m, n):
+    """compulsory bytes per phase (uint32 ids, 4-byte offsets)."""
+    return {
+        "first_occurrence": 8 * m + 4 * n,
+        "compact": m / 2 + 16 * n,
+        "relabel": 16 * m + 4 * n,
+        "coo_to_csr": 16 * m + 4 * n + 4,
+    }
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while running."""
+
+    def __init__(self, index=0, period=0.05):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                getattr(pynvml, "nvmlClocksThrottleReasonHwSlowdown", 0x8): "hw_slowdown",
+                getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+                getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+                getattr(pynvml, "nvmlClocksThrottleReasonSwPowerCap", 0x4): "sw_power_cap",
+                getattr(pynvml, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        for bit, nm in names.items():
+                            if r & bit:
+                                self.reasons.add(nm)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            pass
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "samples": len(self.samples),
+            "reasons": sorted(self.reasons),
+        }
+
+
+# ------------------------------------------------------------- CPU (oracle)
+def host_graph(cfg):
+    """The same synthetic graph on the host, int64 (oracle generator =
+    bit-identical twin of the device generator)."""
+    import oracle
+
+    kind, p, _ = CONFIGS[cfg]
+    n, m = graph_size(cfg)
+    if kind == "rmat":
+        I, J = oracle.rmat_edges(p["scale"], p["ef"], GEN_SEED)
+    else:
+        I, J = oracle.grid_edges(p["rows"], p["cols"])
+    lab = oracle.random_labels(n, LABEL_SEED)
+    return n, lab[I], lab[J]
+
+
+def cpu_pipeline_time(n, I, J, threads):
+    import oracle
+
+    t0 = time.perf_counter()
+    oracle.pipeline(I, J, n, threads=threads)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    cores = len(os.sched_getaffinity(0))
+    n, m = graph_size(args.config)
+    n, I, J = host_graph(args.config)
+    # bound the run: each step is the full graph when K <= 12, else a prefix
+    # of the edge stream (same n) sized so K steps stay within a few minutes
+    step_m = m if args.steps <= 12 else max(1 << 20, int(m * 12 / args.steps))
+    Is, Js = I[:step_m], J[:step_m]
+    for _ in range(min(args.warmup, 1)):
+        cpu_pipeline_time(n, Is, Js, cores)
+    ts = [cpu_pipeline_time(n, Is, Js, cores) for _ in range(args.steps)]
+    t = sum(ts)
+    value = step_m * args.steps / t / 1e9
+    sample = f"{'full graph' if step_m == m else f'first {step_m} edges of the edge stream'} per step, {args.steps} steps"
+    line = {
+        "metric": "BOBA reorder+COO->CSR GEdges/s",
+        "value": round(value, 5),
+        "unit": "GEdges/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config][2] + ", randomly relabelled", "n": n, "m": m},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 5), "unit": "GEdges/s", "cores": cores, "kind": "port",
+                         "sample": sample,
+                         "note": "oracle/boba_oracle.c restates the reference (pure Python + numba); "
+                                 "first-hit uses all cores (reference first_hit_chunked), compaction, "
+                                 "relabel and CSR scatter are single-threaded as in the reference"},
+        "e2e": {"value": round(value, 5), "unit": "GEdges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2306_10410_b200 import _native as N
+    from paper_2306_10410_b200 import device as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    cfg = args.config
+    kind, p, desc = CONFIGS[cfg]
+    n, m = graph_size(cfg)
+
+    # ---- synthetic input, randomly relabelled (reference io.py:294-301)
+    if kind == "rmat":
+        I0, J0 = D.generate_rmat(p["scale"], p["ef"], GEN_SEED + rank, dev)
+    else:
+        I0, J0 = D.generate_grid(p["rows"], p["cols"], dev)
+    lab = torch.from_numpy(oracle.random_labels(n, LABEL_SEED + rank).astype(np.int32)).to(dev)
+    I, J = D.gather(lab, I0), D.gather(lab, J0)
+    del I0, J0
+    torch.cuda.synchronize()
+
+    pipe = D.Pipeline(m, n, dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+    s = D._s()
+    P = D._p
+    lib = N.lib
+    ws = pipe.ws
+    counts_bytes = (n * 4 + 4 + 255) & ~255
+    counts = ws[:counts_bytes].view(torch.int32)
+    rest = ws[counts_bytes:]
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        N.check(lib.boba_first_occurrence(P(I), P(J), m, n, P(pipe.first), 0, s))
+        if ev:
+            ev[1].record(stream)
+        N.check(lib.boba_compact(P(pipe.first), m, n, P(pipe.order), P(pipe.label), None, P(rest), rest.numel(), s))
+        if ev:
+            ev[2].record(stream)
+        N.check(lib.boba_relabel(P(I), P(J), m, n, P(pipe.label), P(pipe.I2), P(pipe.J2), P(counts), s))
+        if ev:
+            ev[3].record(stream)
+        N.check(lib.boba_coo_to_csr(P(pipe.I2), P(pipe.J2), None, m, n, P(counts), P(pipe.offsets),
+                                    P(pipe.indices), None, P(rest), rest.numel(), s))
+        if ev:
+            ev[4].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    phase_names = ["first_occurrence", "compact", "relabel", "coo_to_csr"]
+    phase_ms = {k: [] for k in phase_names}
+    step_ms = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)  # evict L2 between steps (outside the timed events)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            step(ev)
+            torch.cuda.synchronize()
+            for i, k in enumerate(phase_names):
+                phase_ms[k].append(ev[i].elapsed_time(ev[i + 1]))
+            step_ms.append(ev[0].elapsed_time(ev[4]))
+    torch.cuda.synchronize()
+    t_total = sum(step_ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total = float(tt.item())
+        dist.barrier()
+    ms_step = 1e3 * t_total / args.steps
+    value = m * world * args.steps / t_total / 1e9
+
+    # ---- verify the timed output once (cheap device-side invariants)
+    lab_out = pipe.label[:n].to(torch.int64)
+    assert int(pipe.offsets[n].item()) == m
+    assert bool(torch.all(torch.sort(lab_out).values == torch.arange(n, device=dev)))
+
+    # ---- roofline per phase
+    hbm, peak_kind = peaks()
+    ab = alg_bytes(m, n)
+    phases = {}
+    for k in phase_names:
+        t = statistics.mean(phase_ms[k]) / 1e3
+        ach = ab[k] / t / 1e9
+        phases[k] = {"ms": round(t * 1e3, 4), "alg_bytes": int(ab[k]), "gbs": round(ach, 1),
+                     "frac": round(ach / hbm, 4)}
+    dom = max(phase_names, key=lambda k: phases[k]["ms"])
+    total_alg = sum(ab.values())
+    roofline = {
+        "bound": "hbm", "kernel": dom, "achieved": phases[dom]["gbs"], "peak": hbm, "peak_kind": peak_kind,
+        "unit": "GB/s", "frac": phases[dom]["frac"], "traffic": None,
+        "pipeline_frac": round(total_alg / (ms_step / 1e3) / 1e9 / hbm, 4),
+        "pipeline_alg_bytes": int(total_alg), "phases": phases,
+    }
+
+    # ---- SpMV e2e speedup: BOBA (reorder+convert+k SpMV) vs random labels (convert + k SpMV)
+    k_iters = SPMV_ITERS[cfg]
+    x = torch.ones(n, dtype=torch.float32, device=dev)
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    spws = D.spmv_workspace(n, m, dev)
+
+    def time_it(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    off_b, idx_b = pipe.offsets[: n + 1], pipe.indices[:m]
+    t_spmv_boba = time_it(lambda: [D.spmv(off_b, idx_b, x, out=y, ws=spws) for _ in range(k_iters)], 3) / k_iters
+    rnd = {}
+
+    def convert_random():
+        rnd["csr"] = D.coo_to_csr(I, J, n)
+
+    t_conv_rand = time_it(convert_random, 3)
+    off_r, idx_r, _ = rnd["csr"]
+    t_spmv_rand = time_it(lambda: [D.spmv(off_r, idx_r, x, out=y, ws=spws) for _ in range(k_iters)], 3) / k_iters
+    t_reorder = sum(statistics.mean(phase_ms[k]) for k in phase_names[:3])
+    t_convert = statistics.mean(phase_ms["coo_to_csr"])
+    e2e_boba = t_reorder + t_convert + k_iters * t_spmv_boba
+    e2e_rand = t_conv_rand + k_iters * t_spmv_rand
+    spmv_info = {
+        "iters": k_iters, "x": "ones",
+        "spmv_ms_boba": round(t_spmv_boba, 4), "spmv_ms_random": round(t_spmv_rand, 4),
+        "convert_ms_random": round(t_conv_rand, 4), "reorder_ms": round(t_reorder, 4),
+        "convert_ms_boba": round(t_convert, 4),
+        "e2e_ms_boba": round(e2e_boba, 4), "e2e_ms_random": round(e2e_rand, 4),
+        "e2e_speedup_boba_vs_random": round(e2e_rand / e2e_boba, 4),
+        "spmv_gflops_boba": round(2 * m / t_spmv_boba / 1e6, 1),
+    }
+    del rnd
+
+    # ---- end to end through the host-buffer C-ABI entry (pinned buffers)
+    hI = torch.empty(m, dtype=torch.int32, pin_memory=True)
+    hJ = torch.empty(m, dtype=torch.int32, pin_memory=True)
+    hI.copy_(I)
+    hJ.copy_(J)
+    h_order = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_label = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_off = torch.empty(n + 1, dtype=torch.int32, pin_memory=True)
+    h_idx = torch.empty(m, dtype=torch.int32, pin_memory=True)
+    del pipe
+    torch.cuda.empty_cache()
+    hp = D.HostPipeline(m, n)
+    e2e_steps = max(3, min(args.steps, 10))
+    hp.run(hI, hJ, n, h_order, h_label, h_off, h_idx)
+    te = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        hp.run(hI, hJ, n, h_order, h_label, h_off, h_idx)
+        te.append(time.perf_counter() - t0)
+    hp.close()
+    t_e2e = sum(te) / len(te)
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e = {"value": round(m * world / t_e2e / 1e9, 4), "unit": "GEdges/s", "ms_per_step": round(t_e2e * 1e3, 3),
+           "h2d_bytes_per_step": 8 * m, "d2h_bytes_per_step": 4 * n + 4 * n + 4 * (n + 1) + 4 * m,
+           "path": "boba_ctx_reorder_to_csr_host (pinned host uint32 buffers; outputs order, label, CSR)"}
+
+    # ---- CPU baseline on this host (rank 0, N=1 only), same graph
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = len(os.sched_getaffinity(0))
+        hI64 = I.cpu().numpy().view(np.uint32).astype(np.int64)
+        hJ64 = J.cpu().numpy().view(np.uint32).astype(np.int64)
+        ts = []
+        t_start = time.perf_counter()
+        while len(ts) < 3 and (time.perf_counter() - t_start) < 25:
+            ts.append(cpu_pipeline_time(n, hI64, hJ64, cores))
+        tc = statistics.median(ts)
+        cpu = {"value": round(m / tc / 1e9, 5), "unit": "GEdges/s", "cores": cores, "kind": "port",
+               "sample": f"full graph, {len(ts)} runs (median)", "ms": round(tc * 1e3, 1),
+               "note": "oracle/boba_oracle.c (reference restated in C); first-hit on all cores, "
+                       "rest single-threaded as in the reference"}
+
+    launches_per_step = 1 + (1 if m & 3 else 0) + 3 + 1 + (1 + 3 * csr_passes(n))
+    line = {
+        "metric": "BOBA reorder+COO->CSR GEdges/s",
+        "value": round(value, 3),
+        "unit": "GEdges/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": desc + ", randomly relabelled (Graph500 a,b,c=.57,.19,.19; seed 1; labels seed 7)",
+                   "n": n, "m": m, "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "256 MiB L2 flush between steps; inputs 8m bytes > L2"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "spmv": spmv_info,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def csr_passes(n):
+    bits = 0 if n <= 1 else (n - 1).bit_length()
+    maxb = 8 if os.environ.get("BOBA_RADIX_MAX_BITS") == "8" else 11
+    return 0 if bits == 0 else -(-bits // maxb)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

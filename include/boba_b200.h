@@ -1,0 +1,152 @@
+/*
+ * boba_b200.h -- C ABI of the B200-native BOBA hot path (libboba_b200.so).
+ *
+ * This is the drop-in boundary for the reference package's native seam,
+ * pkg/src/boba/_parallel.py ("All hot loops live here behind plain-array
+ * signatures", _parallel.py:1-5), plus the numpy-level structural ops of
+ * graph.py and kernels.py that sit on the same path.  Each entry point names
+ * the reference interface it replaces (file:line relative to
+ * /root/reference/pkg/src/boba/).  Binding recipes (ctypes / cffi) are in
+ * INTEGRATION.md.
+ *
+ * Conventions (all entry points):
+ *   - Vertex ids, positions and CSR offsets are uint32 (n <= 2^32 - 1,
+ *     2m <= 2^32 - 2; the reference uses int64, graph.py:31 -- widen with
+ *     boba_widen_ids).  First-occurrence "unset" is 0xFFFFFFFF (the
+ *     reference's RANK_UNSET = INT64_MAX, _parallel.py:31).
+ *   - Pointers are DEVICE pointers unless the name ends in _host.  Inputs are
+ *     borrowed read-only (the reference never mutates inputs, graph.py:1-8);
+ *     outputs and workspaces are caller-allocated.
+ *   - Work is enqueued on `stream` (a cudaStream_t passed as void*); no
+ *     entry point synchronises the host except the *_host ones.
+ *   - Return 0 on success, a nonzero BOBA_E* code on failure; the message is
+ *     in boba_last_error() (thread-local).  Invalid arguments are reported,
+ *     never silently clamped.
+ *   - Thread-safe across streams and devices (no hidden global state except
+ *     per-device kernel attributes).
+ */
+#ifndef BOBA_B200_H
+#define BOBA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BOBA_OK 0
+#define BOBA_EINVAL 1   /* bad argument (null pointer, size out of range, small workspace) */
+#define BOBA_ECUDA 2    /* CUDA runtime / launch error */
+#define BOBA_ERANGE 3   /* an input id is out of [0, n) (reference MalformedGraphError) */
+#define BOBA_ENOMEM 4   /* device allocation failed (context API) */
+
+#define BOBA_UNSET_U32 0xFFFFFFFFu
+
+/* Library identity and the last error message of the calling thread. */
+int boba_abi_version(void);
+const char *boba_last_error(void);
+
+/* --- Phase 1: first occurrence ------------------------------------------
+ * first[v] = min{ p : (p < m and I[p] == v) or (p >= m and J[p-m] == v) },
+ * BOBA_UNSET_U32 if v never occurs.
+ * Replaces _parallel.first_hit_chunked (_parallel.py:139-162) and the rank
+ * half of first_hit_order_sequential (_parallel.py:111-136).  relaxed != 0
+ * replaces first_hit_racy / run_racy_first_hit (_parallel.py:165-175,44-52):
+ * guarded unsynchronised stores; every first[v] still names a position
+ * holding v, but the minimum may be lost. */
+int boba_first_occurrence(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n,
+                          uint32_t *first, int relaxed, void *stream);
+
+/* --- Phase 2: rank compaction -> permutation --------------------------
+ * order[k] = the vertex with the k-th smallest first[] value, then the
+ * vertices with first == UNSET in ascending id; label[order[k]] = k.
+ * Replaces _parallel.compact_ranks (_parallel.py:178-201) and the label
+ * construction of graph.Permutation (graph.py:205-208).  n_seen (device
+ * scalar, may be NULL) receives the number of vertices that occur. */
+size_t boba_compact_workspace_size(uint64_t m, uint32_t n);
+int boba_compact(const uint32_t *first, uint64_t m, uint32_t n, uint32_t *order, uint32_t *label,
+                 uint32_t *n_seen, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Phase 1 + 2: the deterministic BOBA permutation of ordering.boba_parallel
+ * (ordering.py:99-151; == boba_sequential, ordering.py:59-96).  first
+ * (n uint32) is an output too (the reference's return_ranks array). */
+size_t boba_order_workspace_size(uint64_t m, uint32_t n);
+int boba_order(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n, int relaxed,
+               uint32_t *first, uint32_t *order, uint32_t *label, void *workspace,
+               size_t workspace_bytes, void *stream);
+
+/* --- Phase 3: relabel ---------------------------------------------------
+ * I2[e] = label[I[e]], J2[e] = label[J[e]]; edge order unchanged.
+ * Replaces graph.apply_permutation (graph.py:280-289).  row_counts (n
+ * uint32, may be NULL) additionally receives the out-degree histogram of
+ * the relabelled rows (np.bincount of graph.py:270) for boba_coo_to_csr. */
+int boba_relabel(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n, const uint32_t *label,
+                 uint32_t *I2, uint32_t *J2, uint32_t *row_counts, void *stream);
+
+/* Out-degree histogram: replaces graph.degrees (graph.py:292-294). */
+int boba_degrees(const uint32_t *I, uint64_t m, uint32_t n, uint32_t *deg, void *stream);
+
+/* --- Phase 4: COO -> CSR, reference within-row order -------------------
+ * offsets (n+1) = [0, cumsum(bincount(I2))]; row v of indices holds J2 of
+ * the edges with I2 == v in edge-list order; weights (float64, may be NULL)
+ * move with their edges bit-exactly.  Replaces graph.coo_to_csr
+ * (graph.py:253-277) and _parallel.scatter_rows (_parallel.py:55-88).
+ * row_counts may be NULL (computed) or the histogram from boba_relabel. */
+size_t boba_coo_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted);
+int boba_coo_to_csr(const uint32_t *I2, const uint32_t *J2, const double *weights, uint64_t m,
+                    uint32_t n, const uint32_t *row_counts, uint32_t *offsets, uint32_t *indices,
+                    double *weights_out, void *workspace, size_t workspace_bytes, void *stream);
+
+/* --- Phase 5: SpMV (fp32) -------------------------------------------------
+ * y[v] = sum over row v of weights[k] * x[indices[k]] (weights NULL = 1);
+ * empty rows give 0.  Replaces kernels.spmv_pull (kernels.py:30-52; the
+ * reference accumulates in float64 -- results agree to fp32 rounding).
+ * Deterministic run to run. */
+size_t boba_spmv_workspace_size(uint32_t n, uint64_t m);
+int boba_spmv(const uint32_t *offsets, const uint32_t *indices, const float *weights,
+              const float *x, float *y, uint32_t n, uint64_t m, void *workspace,
+              size_t workspace_bytes, void *stream);
+
+/* --- Fused device pipeline (reference bench.py:135-149: reorder = BOBA +
+ * apply_permutation, convert = coo_to_csr) ------------------------------ */
+size_t boba_reorder_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted);
+int boba_reorder_to_csr(const uint32_t *I, const uint32_t *J, const double *weights, uint64_t m,
+                        uint32_t n, uint32_t *first, uint32_t *order, uint32_t *label, uint32_t *I2,
+                        uint32_t *J2, uint32_t *offsets, uint32_t *indices, double *weights_out,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* --- Host-buffer pipeline (end to end, synchronous) ----------------------
+ * A context owns device buffers for graphs up to (max_m, max_n) on the
+ * current device plus a stream.  boba_ctx_reorder_to_csr_host copies I, J
+ * host -> device, runs the fused pipeline and copies order, label, offsets
+ * and indices back (I2/J2 too when non-NULL).  Host buffers may be pageable
+ * or pinned (pinned is faster). */
+typedef struct boba_ctx boba_ctx;
+int boba_ctx_create(uint64_t max_m, uint32_t max_n, boba_ctx **out);
+void boba_ctx_destroy(boba_ctx *ctx);
+int boba_ctx_reorder_to_csr_host(boba_ctx *ctx, const uint32_t *I_host, const uint32_t *J_host,
+                                 uint64_t m, uint32_t n, uint32_t *order_host, uint32_t *label_host,
+                                 uint32_t *I2_host, uint32_t *J2_host, uint32_t *offsets_host,
+                                 uint32_t *indices_host);
+
+/* --- Plumbing and input generators --------------------------------------- */
+/* int64 -> uint32 with the reference's range check (graph.py:99-106):
+ * returns BOBA_ERANGE and *bad_index (host, may be NULL) = first offending
+ * index if any value is outside [0, bound).  Synchronises `stream`. */
+int boba_narrow_ids(const int64_t *in, uint64_t count, uint64_t bound, uint32_t *out,
+                    int64_t *bad_index, void *stream);
+int boba_widen_ids(const uint32_t *in, uint64_t count, int64_t *out, void *stream);
+/* out[i] = src[idx[i]] (permutation application on vertex arrays). */
+int boba_gather_u32(const uint32_t *src, const uint32_t *idx, uint64_t count, uint32_t *out,
+                    void *stream);
+/* Graph500 R-MAT (a,b,c,d = .57,.19,.19,.05), m = edge_factor << scale
+ * i.i.d. edges in generation order; identical to oracle_rmat_edges. */
+int boba_generate_rmat(int scale, uint64_t m, uint64_t seed, uint32_t *I, uint32_t *J, void *stream);
+/* 4-neighbour grid, reference generators.py:100-111 generate_grid. */
+int boba_generate_grid(uint32_t rows, uint32_t cols, uint32_t *I, uint32_t *J, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BOBA_B200_H */

@@ -1,0 +1,201 @@
+"""CPU oracle for the BOBA hot path -- TEST INFRASTRUCTURE, not product code.
+
+A ctypes view of ``boba_oracle.c``, a plain-C restatement of the reference
+functions on the path (reference ``pkg/src/boba/_parallel.py``, ``graph.py``,
+``kernels.py``; file:line in each C function's comment).  Arrays are int64
+like the reference's (``graph.py:31`` ``INDEX_DTYPE``).
+
+Allowed importers: ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs -- always as the checker or the
+CPU baseline, never as the thing measured for the GPU.  The product package
+``paper_2306_10410_b200`` never imports this module.
+
+Parity pinning: ``tests/test_oracle.py`` checks every function here against
+the golden vectors in ``tests/golden/`` (made by importing the reference,
+``tests/golden/make_golden.py``) and the reference's own known answers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+RANK_UNSET = np.iinfo(np.int64).max  # reference _parallel.py:31
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+
+
+def build() -> str:
+    """Compile liboracle.so with the committed Makefile (gcc + OpenMP)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH) or (
+        os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "boba_oracle.c"))
+    ):
+        build()
+    lib = ctypes.CDLL(_LIB_PATH)
+    sigs = {
+        "oracle_num_threads": ([], ctypes.c_int),
+        "oracle_first_hit_order_sequential": ([_P, _P, _I64, _I64, _P, _P], None),
+        "oracle_first_hit_chunked": ([_P, _P, _I64, _I64, _I64, ctypes.c_int, _P], None),
+        "oracle_compact_ranks": ([_P, _P, _P, _I64, _I64, _P], None),
+        "oracle_label_from_order": ([_P, _I64, _P], None),
+        "oracle_apply_permutation": ([_P, _P, _I64, _P, _P, _P], None),
+        "oracle_degrees": ([_P, _I64, _I64, _P], None),
+        "oracle_coo_to_csr": ([_P, _P, _P, _I64, _I64, _P, _P, _P], None),
+        "oracle_spmv_pull": ([_P, _P, _P, _P, _I64, _P], None),
+        "oracle_rmat_edges": ([ctypes.c_int, _I64, ctypes.c_uint64, _I64, _I64, _P, _P], None),
+        "oracle_grid_edges": ([_I64, _I64, _P, _P], None),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())
+
+
+def first_hit_order_sequential(I, J, n):
+    """reference _parallel.py:111-136 -> (r, order)."""
+    I, J = _i64(I), _i64(J)
+    r = np.empty(n, np.int64)
+    order = np.empty(n, np.int64)
+    _load().oracle_first_hit_order_sequential(_ptr(I), _ptr(J), I.size, n, _ptr(r), _ptr(order))
+    return r, order
+
+
+def first_hit_chunked(I, J, n, nchunks, threads=0):
+    """reference _parallel.py:139-162 -> r."""
+    I, J = _i64(I), _i64(J)
+    r = np.empty(n, np.int64)
+    _load().oracle_first_hit_chunked(_ptr(I), _ptr(J), I.size, n, int(nchunks), int(threads), _ptr(r))
+    return r
+
+
+def compact_ranks(r, I, J):
+    """reference _parallel.py:178-201 -> order."""
+    r, I, J = _i64(r), _i64(I), _i64(J)
+    order = np.empty(r.size, np.int64)
+    _load().oracle_compact_ranks(_ptr(r), _ptr(I), _ptr(J), I.size, r.size, _ptr(order))
+    return order
+
+
+def label_from_order(order):
+    """reference graph.py:205-208 -> label."""
+    order = _i64(order)
+    label = np.empty_like(order)
+    _load().oracle_label_from_order(_ptr(order), order.size, _ptr(label))
+    return label
+
+
+def boba_order(I, J, n):
+    """reference ordering.py:136-140 (deterministic, thread_hint=None)."""
+    return first_hit_order_sequential(I, J, n)[1]
+
+
+def apply_permutation(I, J, label):
+    """reference graph.py:280-289 -> (I2, J2)."""
+    I, J, label = _i64(I), _i64(J), _i64(label)
+    I2 = np.empty_like(I)
+    J2 = np.empty_like(J)
+    _load().oracle_apply_permutation(_ptr(I), _ptr(J), I.size, _ptr(label), _ptr(I2), _ptr(J2))
+    return I2, J2
+
+
+def degrees(I, n):
+    """reference graph.py:292-294."""
+    I = _i64(I)
+    d = np.empty(n, np.int64)
+    _load().oracle_degrees(_ptr(I), I.size, n, _ptr(d))
+    return d
+
+
+def coo_to_csr(I, J, n, weights=None):
+    """reference graph.py:253-277 + _parallel.py:55-88 -> (offsets, indices, weights)."""
+    I, J = _i64(I), _i64(J)
+    W = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    offsets = np.empty(n + 1, np.int64)
+    indices = np.empty(I.size, np.int64)
+    W2 = None if W is None else np.empty(I.size, np.float64)
+    _load().oracle_coo_to_csr(_ptr(I), _ptr(J), _ptr(W), I.size, n, _ptr(offsets), _ptr(indices), _ptr(W2))
+    return offsets, indices, W2
+
+
+def spmv_pull(offsets, indices, x, weights=None):
+    """reference kernels.py:30-52 (sequential row sums, fp64)."""
+    offsets, indices = _i64(offsets), _i64(indices)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    W = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    n = offsets.size - 1
+    y = np.empty(n, np.float64)
+    _load().oracle_spmv_pull(_ptr(offsets), _ptr(indices), _ptr(W), _ptr(x), n, _ptr(y))
+    return y
+
+
+def rmat_edges(scale, edge_factor, seed, e0=0, e1=None):
+    """Host twin of the device R-MAT generator (input prep, not reference)."""
+    m = edge_factor << scale
+    e1 = m if e1 is None else e1
+    I = np.empty(e1 - e0, np.int64)
+    J = np.empty(e1 - e0, np.int64)
+    _load().oracle_rmat_edges(int(scale), m, int(seed) & (2**64 - 1), e0, e1, _ptr(I), _ptr(J))
+    return I, J
+
+
+def grid_edges(rows, cols):
+    """reference generators.py:100-111 generate_grid (I, J)."""
+    m = 2 * rows * (cols - 1) + 2 * (rows - 1) * cols
+    I = np.empty(m, np.int64)
+    J = np.empty(m, np.int64)
+    _load().oracle_grid_edges(rows, cols, _ptr(I), _ptr(J))
+    return I, J
+
+
+def random_labels(n, seed):
+    """reference ordering.py:154-157 random_order / io.py:294-301
+    randomize_labels: order = default_rng(seed).permutation(n); returns the
+    label (inverse) array that relabels the graph."""
+    order = np.random.default_rng(seed).permutation(n).astype(np.int64)
+    return label_from_order(order)
+
+
+def pipeline(I, J, n, threads=0, weights=None):
+    """The reference bench's reorder + convert phases (bench.py:135-149) with
+    the reference's threading: first_hit_chunked over `threads` chunks when
+    threads > 1 (ordering.py:141-143), else the fused sequential pass.
+    Returns (order, label, I2, J2, offsets, indices, weights2)."""
+    if threads and threads > 1:
+        r = first_hit_chunked(I, J, n, threads, threads)
+        order = compact_ranks(r, I, J)
+    else:
+        order = first_hit_order_sequential(I, J, n)[1]
+    label = label_from_order(order)
+    I2, J2 = apply_permutation(I, J, label)
+    offsets, indices, w2 = coo_to_csr(I2, J2, n, weights)
+    return order, label, I2, J2, offsets, indices, w2

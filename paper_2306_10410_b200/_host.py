@@ -1,0 +1,103 @@
+"""numpy <-> device glue for the reference-shaped API.
+
+The reference works on host int64 arrays; the kernels on device uint32.
+Each helper copies its inputs to the current CUDA device once, narrows them
+there (with the reference's [0, n) range check), runs the C-ABI phase and
+widens the results back to int64 on the device before a single D2H copy.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import device as D
+
+RANK_UNSET = np.iinfo(np.int64).max  # reference _parallel.py:31
+
+
+def _dev():
+    return D.require_cuda()
+
+
+def to_device_ids(a, bound: int, name: str = "ids") -> torch.Tensor:
+    arr = np.ascontiguousarray(a, dtype=np.int64)
+    t = torch.from_numpy(arr).to(_dev())
+    return D.narrow_ids(t, bound, name)
+
+
+def to_host_ids(t: torch.Tensor) -> np.ndarray:
+    if t.numel() == 0:
+        return np.empty(0, dtype=np.int64)
+    return D.as_u32_to_i64(t).cpu().numpy()
+
+
+def first_to_ranks(first: torch.Tensor) -> np.ndarray:
+    """uint32 first-occurrence array -> the reference's int64 rank array
+    (0xFFFFFFFF -> RANK_UNSET)."""
+    r = to_host_ids(first)
+    r[r == 0xFFFFFFFF] = RANK_UNSET
+    return r
+
+
+def ranks_to_first(r) -> torch.Tensor:
+    r = np.ascontiguousarray(r, dtype=np.int64)
+    f = np.where(r == RANK_UNSET, 0xFFFFFFFF, r).astype(np.uint32).view(np.int32)
+    return torch.from_numpy(f).to(_dev())
+
+
+def boba(I, J, n: int, relaxed: bool = False):
+    """-> (r int64 with RANK_UNSET, order int64, label int64)."""
+    if n == 0:
+        e = np.empty(0, dtype=np.int64)
+        return e, e.copy(), e.copy()
+    dI, dJ = to_device_ids(I, n, "I"), to_device_ids(J, n, "J")
+    first, order, label = D.boba_order(dI, dJ, n, relaxed)
+    return first_to_ranks(first), to_host_ids(order), to_host_ids(label)
+
+
+def compact(r, I, J, n: int):
+    """reference _parallel.compact_ranks on the GPU -> order int64."""
+    if n == 0:
+        return np.empty(0, dtype=np.int64)
+    first = ranks_to_first(r)
+    order, _ = D.compact(first, int(np.asarray(I).size), n)
+    return to_host_ids(order)
+
+
+def relabel(I, J, label, n: int):
+    m = int(np.asarray(I).size)
+    if m == 0:
+        return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.int64)
+    dI, dJ = to_device_ids(I, n, "I"), to_device_ids(J, n, "J")
+    dl = to_device_ids(label, max(n, 1), "label")
+    I2, J2 = D.relabel(dI, dJ, dl, n)
+    return to_host_ids(I2), to_host_ids(J2)
+
+
+def degrees(I, n: int) -> np.ndarray:
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    dI = to_device_ids(I, n, "I")
+    return to_host_ids(D.degrees(dI, n))
+
+
+def coo_to_csr(I, J, n: int, weights=None):
+    dI, dJ = to_device_ids(I, n, "I"), to_device_ids(J, n, "J")
+    w = None
+    if weights is not None:
+        w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(_dev())
+    offsets, indices, w_out = D.coo_to_csr(dI, dJ, n, w)
+    return to_host_ids(offsets), to_host_ids(indices), (None if w_out is None else w_out.cpu().numpy())
+
+
+def spmv(offsets, indices, x, weights=None) -> np.ndarray:
+    n = int(np.asarray(offsets).size) - 1
+    dev = _dev()
+    m = int(np.asarray(indices).size)
+    do = to_device_ids(offsets, m + 1, "offsets")
+    di = to_device_ids(indices, max(n, 1), "indices") if m else torch.empty(0, dtype=D.ID, device=dev)
+    dx = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+    dw = None if weights is None else torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float32)).to(dev)
+    y = D.spmv(do, di, dx, dw)
+    return y.cpu().numpy().astype(np.float64)

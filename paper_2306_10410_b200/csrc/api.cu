@@ -1,0 +1,274 @@
+// extern "C" boundary of libboba_b200.so -- see include/boba_b200.h for the
+// contract and the reference interface each entry point replaces.
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/boba_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return BOBA_OK;
+    if (e == cudaErrorInvalidValue) return fail(BOBA_EINVAL, "%s: invalid value (workspace too small?)", what);
+    return fail(BOBA_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int num_sms() {
+    static thread_local int dev = -1, sms = 148;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d != dev) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+        dev = d;
+    }
+    return sms;
+}
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+int check_sizes(uint64_t m, uint32_t n, const char* what) {
+    if (2 * m > 0xFFFFFFFEull) return fail(BOBA_EINVAL, "%s: 2m = %llu exceeds the uint32 position space", what,
+                                           (unsigned long long)(2 * m));
+    if (n == 0xFFFFFFFFu) return fail(BOBA_EINVAL, "%s: n must be < 2^32 - 1", what);
+    return BOBA_OK;
+}
+
+#define REQUIRE(cond, ...)                                  \
+    do {                                                    \
+        if (!(cond)) return fail(BOBA_EINVAL, __VA_ARGS__); \
+    } while (0)
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct boba_ctx {
+    int device = 0;
+    uint64_t max_m = 0;
+    uint32_t max_n = 0;
+    cudaStream_t stream = nullptr;
+    uint32_t *I = nullptr, *J = nullptr, *I2 = nullptr, *J2 = nullptr, *indices = nullptr;
+    uint32_t *first = nullptr, *order = nullptr, *label = nullptr, *offsets = nullptr;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+};
+
+extern "C" {
+
+int boba_abi_version(void) { return 1; }
+const char* boba_last_error(void) { return g_err.c_str(); }
+
+int boba_first_occurrence(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
+                          int relaxed, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_first_occurrence")) return rc;
+    REQUIRE(first || n == 0, "boba_first_occurrence: first is NULL");
+    REQUIRE((I && J) || m == 0, "boba_first_occurrence: I/J is NULL");
+    if (n == 0) return BOBA_OK;
+    return cuda_status(boba::launch_first_hit(I, J, m, n, first, relaxed != 0, num_sms(), S(stream)),
+                       "boba_first_occurrence");
+}
+
+size_t boba_compact_workspace_size(uint64_t m, uint32_t n) { return boba::compact_workspace_bytes(m, n); }
+
+int boba_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order, uint32_t* label,
+                 uint32_t* n_seen, void* ws, size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_compact")) return rc;
+    if (n == 0) return BOBA_OK;
+    REQUIRE(first && order && label && ws, "boba_compact: NULL argument");
+    return cuda_status(boba::launch_compact(first, m, n, order, label, n_seen, ws, ws_bytes, num_sms(), S(stream)),
+                       "boba_compact");
+}
+
+size_t boba_order_workspace_size(uint64_t m, uint32_t n) { return boba::compact_workspace_bytes(m, n); }
+
+int boba_order(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, int relaxed, uint32_t* first,
+               uint32_t* order, uint32_t* label, void* ws, size_t ws_bytes, void* stream) {
+    if (int rc = boba_first_occurrence(I, J, m, n, first, relaxed, stream)) return rc;
+    return boba_compact(first, m, n, order, label, nullptr, ws, ws_bytes, stream);
+}
+
+int boba_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, const uint32_t* label, uint32_t* I2,
+                 uint32_t* J2, uint32_t* row_counts, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_relabel")) return rc;
+    REQUIRE((I && J && I2 && J2 && label) || m == 0, "boba_relabel: NULL argument");
+    return cuda_status(boba::launch_relabel(I, J, m, label, I2, J2, row_counts, n, num_sms(), S(stream)),
+                       "boba_relabel");
+}
+
+int boba_degrees(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* deg, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_degrees")) return rc;
+    if (n == 0) return BOBA_OK;
+    REQUIRE(deg && (I || m == 0), "boba_degrees: NULL argument");
+    return cuda_status(boba::launch_hist(I, m, n, deg, num_sms(), S(stream)), "boba_degrees");
+}
+
+size_t boba_coo_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted) {
+    return boba::coo_to_csr_workspace_bytes(m, n, weighted != 0);
+}
+
+int boba_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
+                    const uint32_t* row_counts, uint32_t* offsets, uint32_t* indices, double* w_out, void* ws,
+                    size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_coo_to_csr")) return rc;
+    REQUIRE(offsets && ws, "boba_coo_to_csr: NULL offsets/workspace");
+    REQUIRE((I2 && J2 && indices) || m == 0, "boba_coo_to_csr: NULL edge arrays");
+    REQUIRE(!w || w_out || m == 0, "boba_coo_to_csr: weights given but weights_out is NULL");
+    return cuda_status(boba::launch_coo_to_csr(I2, J2, w, m, n, row_counts, offsets, indices, w_out, ws, ws_bytes,
+                                               num_sms(), S(stream)),
+                       "boba_coo_to_csr");
+}
+
+size_t boba_spmv_workspace_size(uint32_t n, uint64_t m) { return boba::spmv_workspace_bytes(n, m); }
+
+int boba_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y, uint32_t n,
+              uint64_t m, void* ws, size_t ws_bytes, void* stream) {
+    if (n == 0) return BOBA_OK;
+    REQUIRE(offsets && x && y && ws && (indices || m == 0), "boba_spmv: NULL argument");
+    REQUIRE((uint64_t)n + m < 0xFFFFFFFFull * 2048ull, "boba_spmv: too large");
+    return cuda_status(boba::launch_spmv(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream)), "boba_spmv");
+}
+
+size_t boba_reorder_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted) {
+    size_t a = boba::compact_workspace_bytes(m, n);
+    size_t b = boba::coo_to_csr_workspace_bytes(m, n, weighted != 0);
+    return align256((size_t)n * 4 + 4) + (a > b ? a : b);
+}
+
+int boba_reorder_to_csr(const uint32_t* I, const uint32_t* J, const double* w, uint64_t m, uint32_t n,
+                        uint32_t* first, uint32_t* order, uint32_t* label, uint32_t* I2, uint32_t* J2,
+                        uint32_t* offsets, uint32_t* indices, double* w_out, void* ws, size_t ws_bytes,
+                        void* stream) {
+    if (int rc = check_sizes(m, n, "boba_reorder_to_csr")) return rc;
+    REQUIRE(ws_bytes >= boba_reorder_to_csr_workspace_size(m, n, w != nullptr),
+            "boba_reorder_to_csr: workspace too small");
+    if (n == 0) return BOBA_OK;
+    uint32_t* counts = static_cast<uint32_t*>(ws);
+    void* rest = static_cast<char*>(ws) + align256((size_t)n * 4 + 4);
+    size_t rest_bytes = ws_bytes - align256((size_t)n * 4 + 4);
+    if (int rc = boba_first_occurrence(I, J, m, n, first, 0, stream)) return rc;
+    if (int rc = boba_compact(first, m, n, order, label, nullptr, rest, rest_bytes, stream)) return rc;
+    if (int rc = boba_relabel(I, J, m, n, label, I2, J2, counts, stream)) return rc;
+    return boba_coo_to_csr(I2, J2, w, m, n, counts, offsets, indices, w_out, rest, rest_bytes, stream);
+}
+
+int boba_ctx_create(uint64_t max_m, uint32_t max_n, boba_ctx** out) {
+    REQUIRE(out, "boba_ctx_create: out is NULL");
+    if (int rc = check_sizes(max_m, max_n, "boba_ctx_create")) return rc;
+    boba_ctx* c = new boba_ctx();
+    c->max_m = max_m;
+    c->max_n = max_n;
+    cudaGetDevice(&c->device);
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    const size_t mb = max_m * 4 + 16, nb = (size_t)max_n * 4 + 16;
+    c->ws_bytes = boba_reorder_to_csr_workspace_size(max_m, max_n, 0);
+    if (e == cudaSuccess) e = cudaMalloc(&c->I, mb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->J, mb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->I2, mb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->J2, mb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->indices, mb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->first, nb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->order, nb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->label, nb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->offsets, nb + 4);
+    if (e == cudaSuccess) e = cudaMalloc(&c->ws, c->ws_bytes);
+    if (e != cudaSuccess) {
+        boba_ctx_destroy(c);
+        return fail(BOBA_ENOMEM, "boba_ctx_create: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return BOBA_OK;
+}
+
+void boba_ctx_destroy(boba_ctx* c) {
+    if (!c) return;
+    for (void* p : {(void*)c->I, (void*)c->J, (void*)c->I2, (void*)c->J2, (void*)c->indices, (void*)c->first,
+                    (void*)c->order, (void*)c->label, (void*)c->offsets, c->ws})
+        if (p) cudaFree(p);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int boba_ctx_reorder_to_csr_host(boba_ctx* c, const uint32_t* I_h, const uint32_t* J_h, uint64_t m, uint32_t n,
+                                 uint32_t* order_h, uint32_t* label_h, uint32_t* I2_h, uint32_t* J2_h,
+                                 uint32_t* offsets_h, uint32_t* indices_h) {
+    REQUIRE(c, "boba_ctx_reorder_to_csr_host: NULL context");
+    REQUIRE(m <= c->max_m && n <= c->max_n, "boba_ctx_reorder_to_csr_host: graph exceeds the context capacity");
+    REQUIRE(order_h && label_h && offsets_h && (indices_h || m == 0) && ((I_h && J_h) || m == 0),
+            "boba_ctx_reorder_to_csr_host: NULL host buffer");
+    cudaStream_t s = c->stream;
+    cudaError_t e = cudaSuccess;
+    if (m) e = cudaMemcpyAsync(c->I, I_h, m * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(c->J, J_h, m * 4, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "boba_ctx_reorder_to_csr_host: H2D");
+    if (int rc = boba_reorder_to_csr(c->I, c->J, nullptr, m, n, c->first, c->order, c->label, c->I2, c->J2,
+                                     c->offsets, c->indices, nullptr, c->ws, c->ws_bytes, s))
+        return rc;
+    e = cudaMemcpyAsync(order_h, c->order, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(label_h, c->label, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(offsets_h, c->offsets, ((size_t)n + 1) * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(indices_h, c->indices, m * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && I2_h && m) e = cudaMemcpyAsync(I2_h, c->I2, m * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && J2_h && m) e = cudaMemcpyAsync(J2_h, c->J2, m * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return cuda_status(e, "boba_ctx_reorder_to_csr_host");
+}
+
+int boba_narrow_ids(const int64_t* in, uint64_t count, uint64_t bound, uint32_t* out, int64_t* bad_index,
+                    void* stream) {
+    REQUIRE((in && out) || count == 0, "boba_narrow_ids: NULL argument");
+    REQUIRE(bound <= 0xFFFFFFFFull, "boba_narrow_ids: bound exceeds uint32");
+    if (count == 0) return BOBA_OK;
+    unsigned long long* d_bad = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_bad, 8, S(stream));
+    if (e == cudaSuccess) e = boba::launch_narrow(in, count, bound, out, d_bad, num_sms(), S(stream));
+    unsigned long long h_bad = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h_bad, d_bad, 8, cudaMemcpyDeviceToHost, S(stream));
+    if (d_bad) cudaFreeAsync(d_bad, S(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+    if (e != cudaSuccess) return cuda_status(e, "boba_narrow_ids");
+    if (h_bad != ~0ull) {
+        if (bad_index) *bad_index = (int64_t)h_bad;
+        return fail(BOBA_ERANGE, "boba_narrow_ids: element %llu out of range [0, %llu)", h_bad,
+                    (unsigned long long)bound);
+    }
+    return BOBA_OK;
+}
+
+int boba_widen_ids(const uint32_t* in, uint64_t count, int64_t* out, void* stream) {
+    REQUIRE((in && out) || count == 0, "boba_widen_ids: NULL argument");
+    return cuda_status(boba::launch_widen(in, count, out, num_sms(), S(stream)), "boba_widen_ids");
+}
+
+int boba_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, void* stream) {
+    REQUIRE((src && idx && out) || count == 0, "boba_gather_u32: NULL argument");
+    return cuda_status(boba::launch_gather_u32(src, idx, count, out, num_sms(), S(stream)), "boba_gather_u32");
+}
+
+int boba_generate_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32_t* J, void* stream) {
+    REQUIRE(scale >= 0 && scale <= 32, "boba_generate_rmat: scale out of range");
+    REQUIRE((I && J) || m == 0, "boba_generate_rmat: NULL argument");
+    return cuda_status(boba::launch_rmat(scale, m, seed, I, J, num_sms(), S(stream)), "boba_generate_rmat");
+}
+
+int boba_generate_grid(uint32_t rows, uint32_t cols, uint32_t* I, uint32_t* J, void* stream) {
+    REQUIRE(rows >= 1 && cols >= 1, "boba_generate_grid: dimensions must be positive");
+    REQUIRE(I && J, "boba_generate_grid: NULL argument");
+    return cuda_status(boba::launch_grid(rows, cols, I, J, num_sms(), S(stream)), "boba_generate_grid");
+}
+
+}  // extern "C"

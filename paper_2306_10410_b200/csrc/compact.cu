@@ -1,0 +1,208 @@
+// Phase 2 -- rank compaction: first[] -> (order, label), linear time, no sort.
+//
+// Reference: pkg/src/boba/_parallel.py:178-201 compact_ranks (presence flag
+// per used rank over [0,2m), compaction scan, isolated vertices appended in
+// ascending ID order) and graph.py:205-208 (label[order[k]] = k).
+//
+// B200 formulation (three kernels, all O(n) random or O(m/32) streaming):
+//   k_mark          one bit per used position: atomicOr into a 2m-bit map.
+//   k_sector_scan   single-pass decoupled-lookback exclusive scan of the
+//                   popcount of every 256-bit sector -> secprefix[]; the
+//                   total is n_seen (vertices that occur at all).
+//   k_assign        per vertex: rank = secprefix[sector] + popcount of the
+//                   bits below it inside its (one 32-byte) sector, or, for a
+//                   vertex that never occurs, n_seen + its rank among the
+//                   isolated vertices (a second lookback scan over vertex
+//                   tiles keeps them in ascending ID order).  Writes
+//                   label[v] = rank (coalesced) and order[rank] = v.
+// No gather of I||J is needed: position first[v] holds v by definition.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace boba {
+
+constexpr int kScanNT = 256;
+constexpr int kSectorsPerThread = 4;                    // 4 x 32 B per thread
+constexpr int kSectorsPerTile = kScanNT * kSectorsPerThread;
+constexpr int kAssignVPT = 4;                           // vertices per thread
+constexpr int kAssignTile = kScanNT * kAssignVPT;
+
+__global__ void k_mark(const uint32_t* __restrict__ first, uint32_t n, uint32_t* bits) {
+    uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+        uint32_t f = __ldg(first + v);
+        if (f != BOBA_UNSET) atomicOr(bits + (f >> 5), 1u << (f & 31));
+    }
+}
+
+__global__ void __launch_bounds__(kScanNT) k_sector_scan(const uint4* __restrict__ bits, uint64_t sectors,
+                                                         uint32_t* secprefix, unsigned long long* status,
+                                                         unsigned* tile_counter, uint32_t* n_seen) {
+    __shared__ unsigned s_tile;
+    __shared__ uint32_t s_scan[kScanNT / 32 + 1];
+    __shared__ unsigned long long s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t s0 = tile * kSectorsPerTile + (uint64_t)threadIdx.x * kSectorsPerThread;
+    uint32_t cnt[kSectorsPerThread];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kSectorsPerThread; k++) {
+        uint32_t c = 0;
+        if (s0 + k < sectors) {
+            uint4 a = bits[2 * (s0 + k)], b = bits[2 * (s0 + k) + 1];
+            c = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) +
+                __popc(b.z) + __popc(b.w);
+        }
+        cnt[k] = c;
+        sum += c;
+    }
+    uint32_t total;
+    uint32_t excl_thread = block_exclusive_sum<kScanNT>(sum, s_scan, &total);
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0)
+            st_volatile_u64(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | (unsigned long long)total);
+        unsigned long long ex = tile == 0 ? 0ull : warp_lookback(status, (long long)tile);
+        if (threadIdx.x == 0) {
+            if (tile != 0) st_volatile_u64(status + tile, kFlagInc | (ex + total));
+            s_excl = ex;
+            uint64_t ntiles = ceil_div(sectors, kSectorsPerTile);
+            if (tile == ntiles - 1) *n_seen = (uint32_t)(ex + total);
+        }
+    }
+    __syncthreads();
+    uint32_t run = (uint32_t)s_excl + excl_thread;
+#pragma unroll
+    for (int k = 0; k < kSectorsPerThread; k++) {
+        if (s0 + k < sectors) secprefix[s0 + k] = run;
+        run += cnt[k];
+    }
+}
+
+__device__ __forceinline__ uint32_t rank_of(uint32_t f, const uint4* __restrict__ bits,
+                                            const uint32_t* __restrict__ secprefix) {
+    const uint32_t s = f >> 8, w = (f >> 5) & 7, b = f & 31;
+    uint4 lo = __ldg(bits + 2 * s), hi = __ldg(bits + 2 * s + 1);
+    uint32_t words[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t r = __ldg(secprefix + s);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        if ((uint32_t)k < w) r += __popc(words[k]);
+        else if ((uint32_t)k == w) r += __popc(words[k] & ((1u << b) - 1u));
+    }
+    return r;
+}
+
+__global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__ first, uint32_t n,
+                                                    const uint4* __restrict__ bits,
+                                                    const uint32_t* __restrict__ secprefix,
+                                                    const uint32_t* __restrict__ n_seen_ptr,
+                                                    uint32_t* order, uint32_t* label,
+                                                    unsigned long long* status, unsigned* tile_counter) {
+    __shared__ unsigned s_tile;
+    __shared__ uint32_t s_scan[kScanNT / 32 + 1];
+    __shared__ unsigned long long s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t v0 = tile * kAssignTile + (uint64_t)threadIdx.x * kAssignVPT;
+    uint32_t f[kAssignVPT];
+    uint32_t iso = 0;
+#pragma unroll
+    for (int k = 0; k < kAssignVPT; k++) {
+        f[k] = (v0 + k < n) ? __ldg(first + v0 + k) : 0u;
+        iso += (v0 + k < n && f[k] == BOBA_UNSET);
+    }
+    uint32_t total;
+    uint32_t iso_excl = block_exclusive_sum<kScanNT>(iso, s_scan, &total);
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0)
+            st_volatile_u64(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | (unsigned long long)total);
+        unsigned long long ex = tile == 0 ? 0ull : warp_lookback(status, (long long)tile);
+        if (threadIdx.x == 0) {
+            if (tile != 0) st_volatile_u64(status + tile, kFlagInc | (ex + total));
+            s_excl = ex;
+        }
+    }
+    __syncthreads();
+    uint32_t iso_rank = __ldg(n_seen_ptr) + (uint32_t)s_excl + iso_excl;
+    uint32_t lab[kAssignVPT];
+#pragma unroll
+    for (int k = 0; k < kAssignVPT; k++) {
+        if (v0 + k >= n) continue;
+        uint32_t r = (f[k] == BOBA_UNSET) ? iso_rank++ : rank_of(f[k], bits, secprefix);
+        lab[k] = r;
+        order[r] = (uint32_t)(v0 + k);
+    }
+    if (v0 + kAssignVPT <= n && (reinterpret_cast<uintptr_t>(label) & 15) == 0) {
+        *reinterpret_cast<uint4*>(label + v0) = make_uint4(lab[0], lab[1], lab[2], lab[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kAssignVPT; k++)
+            if (v0 + k < n) label[v0 + k] = lab[k];
+    }
+}
+
+namespace {
+struct CompactWs {
+    uint32_t* bits;
+    uint32_t* secprefix;
+    unsigned long long* st_sec;
+    unsigned long long* st_v;
+    unsigned* counters;
+    size_t total;
+};
+CompactWs carve_compact(void* base, uint64_t m, uint32_t n) {
+    const uint64_t sectors = ceil_div(2 * m, 256) + 1;
+    const uint64_t sec_tiles = ceil_div(sectors, kSectorsPerTile);
+    const uint64_t v_tiles = ceil_div((uint64_t)n, kAssignTile) + 1;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~size_t(255);
+        return base ? static_cast<char*>(base) + o : nullptr;
+    };
+    CompactWs w;
+    w.bits = (uint32_t*)take(sectors * 32);
+    w.st_sec = (unsigned long long*)take(sec_tiles * 8);
+    w.st_v = (unsigned long long*)take(v_tiles * 8);
+    w.counters = (unsigned*)take(64);
+    w.secprefix = (uint32_t*)take(sectors * 4);  // last: not cleared
+    w.total = off;
+    return w;
+}
+}  // namespace
+
+size_t compact_workspace_bytes(uint64_t m, uint32_t n) { return carve_compact(nullptr, m, n).total; }
+
+cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order,
+                           uint32_t* label, uint32_t* n_seen_out, void* ws, size_t ws_bytes,
+                           int num_sms, cudaStream_t s) {
+    if (ws_bytes < compact_workspace_bytes(m, n)) return cudaErrorInvalidValue;
+    if (n == 0) return cudaSuccess;
+    const uint64_t sectors = ceil_div(2 * m, 256) + 1;
+    const uint64_t sec_tiles = ceil_div(sectors, kSectorsPerTile);
+    const uint64_t v_tiles = ceil_div((uint64_t)n, kAssignTile);
+    CompactWs w = carve_compact(ws, m, n);
+    uint32_t* bits = w.bits;
+    uint32_t* secprefix = w.secprefix;
+    unsigned* counters = w.counters;
+    uint32_t* n_seen = counters + 4;
+    // clear bits, lookback status and counters (everything before secprefix)
+    cudaError_t err = cudaMemsetAsync(ws, 0, reinterpret_cast<char*>(secprefix) - static_cast<char*>(ws), s);
+    if (err != cudaSuccess) return err;
+    {
+        uint64_t blocks = ceil_div(n, 256);
+        uint64_t cap = (uint64_t)num_sms * 16;
+        k_mark<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(first, n, bits);
+    }
+    k_sector_scan<<<(int)sec_tiles, kScanNT, 0, s>>>(reinterpret_cast<const uint4*>(bits), sectors,
+                                                     secprefix, w.st_sec, counters + 0, n_seen);
+    k_assign<<<(int)v_tiles, kScanNT, 0, s>>>(first, n, reinterpret_cast<const uint4*>(bits), secprefix,
+                                              n_seen, order, label, w.st_v, counters + 1);
+    if (n_seen_out) cudaMemcpyAsync(n_seen_out, n_seen, 4, cudaMemcpyDeviceToDevice, s);
+    return cudaGetLastError();
+}
+
+}  // namespace boba

@@ -1,0 +1,40 @@
+// Host-side launchers of the BOBA kernels (internal; the public surface is
+// the C ABI in include/boba_b200.h, implemented in api.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace boba {
+
+cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
+                             bool relaxed, int num_sms, cudaStream_t s);
+
+size_t compact_workspace_bytes(uint64_t m, uint32_t n);
+cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order, uint32_t* label,
+                           uint32_t* n_seen_out, void* ws, size_t ws_bytes, int num_sms, cudaStream_t s);
+
+cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label, uint32_t* I2,
+                           uint32_t* J2, uint32_t* counts, uint32_t n, int num_sms, cudaStream_t s);
+
+cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* counts, int num_sms, cudaStream_t s);
+cudaError_t launch_row_offsets(const uint32_t* counts, uint32_t n, uint32_t* offsets, unsigned long long* status,
+                               unsigned* counter, cudaStream_t s);
+size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool weighted);
+cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
+                              const uint32_t* counts_in, uint32_t* offsets, uint32_t* indices, double* w_out,
+                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s);
+
+size_t spmv_workspace_bytes(uint32_t n, uint64_t m);
+cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,
+                        uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s);
+
+cudaError_t launch_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32_t* J, int num_sms, cudaStream_t s);
+cudaError_t launch_grid(uint32_t rows, uint32_t cols, uint32_t* I, uint32_t* J, int num_sms, cudaStream_t s);
+cudaError_t launch_narrow(const int64_t* in, uint64_t count, uint64_t bound, uint32_t* out,
+                          unsigned long long* first_bad, int num_sms, cudaStream_t s);
+cudaError_t launch_widen(const uint32_t* in, uint64_t count, int64_t* out, int num_sms, cudaStream_t s);
+cudaError_t launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, int num_sms,
+                              cudaStream_t s);
+
+}  // namespace boba

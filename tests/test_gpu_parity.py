@@ -1,0 +1,284 @@
+"""GPU parity: every phase of the B200 path against the reference's outputs.
+
+Golden fixtures (made by running the reference, tests/golden/) pin the small
+cases bit-exactly; the C oracle (oracle/, itself pinned by test_oracle.py)
+pins seeded R-MAT / grid graphs up to scale 20; size-independent properties
+cover the full BASELINE sizes.  Integer outputs are compared bit-exactly;
+SpMV (fp32 on the device vs the reference's fp64) within rtol 1e-5 for
+non-negative x, exactly for integer-valued data.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RANK_UNSET = np.iinfo(np.int64).max
+SPMV_RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def bb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2306_10410_b200 as bb
+
+    return bb
+
+
+def run_case(bb, c):
+    g = bb.CooGraph(c["n"], c["I"], c["J"], c["w"])
+    p, r = bb.boba_parallel(g, return_ranks=True)
+    assert np.array_equal(p.order, c["order"]), "order"
+    assert np.array_equal(p.label, c["label"]), "label"
+    assert np.array_equal(r, c["r"]), "ranks"
+    g2 = bb.apply_permutation(g, p)
+    assert np.array_equal(g2.I, c["I2"]) and np.array_equal(g2.J, c["J2"]), "relabel"
+    csr = bb.coo_to_csr(g2)
+    assert np.array_equal(csr.offsets, c["offsets"]), "offsets"
+    assert np.array_equal(csr.indices, c["indices"]), "indices"
+    raw = bb.coo_to_csr(g)
+    assert np.array_equal(raw.offsets, c["offsets_raw"]) and np.array_equal(raw.indices, c["indices_raw"])
+    if c["w"] is not None:
+        assert np.array_equal(csr.weights, c["w2"]) and np.array_equal(raw.weights, c["w2_raw"])
+    assert np.array_equal(bb.degrees(g), c["deg"])
+    y = bb.spmv_pull(csr, c["x"])
+    np.testing.assert_allclose(y, c["y"], rtol=SPMV_RTOL, atol=1e-6)
+    y0 = bb.spmv_pull(raw, c["x"])
+    np.testing.assert_allclose(y0, c["y_raw"], rtol=SPMV_RTOL, atol=1e-6)
+
+
+def test_known_answers(bb, kat):
+    for c in kat:
+        run_case(bb, c)
+
+
+def test_fuzz(bb, fuzz):
+    for c in fuzz:
+        run_case(bb, c)
+
+
+def test_medium(bb, medium):
+    for c in medium:
+        run_case(bb, c)
+
+
+def test_thread_hint_never_changes_the_answer(bb, medium):
+    c = medium.case(2)
+    g = bb.CooGraph(c["n"], c["I"], c["J"])
+    for t in (None, 1, 2, 8):
+        assert np.array_equal(bb.boba_parallel(g, thread_hint=t).order, c["order"])
+    assert np.array_equal(bb.compute_ordering(g, "boba", thread_hint=4).order, c["order"])
+
+
+def test_relaxed_mode_invariants(bb, fuzz, medium):
+    # reference test_ordering.py:79-111 / test_acceptance.py:152-184
+    cases = [fuzz.case(i) for i in range(0, fuzz.count, 7)] + list(medium)
+    for c in cases:
+        g = bb.CooGraph(c["n"], c["I"], c["J"])
+        p, r = bb.boba_parallel(g, mode="relaxed", thread_hint=8, return_ranks=True)
+        assert p.is_valid()
+        flat = np.concatenate([c["I"], c["J"]])
+        present = np.zeros(g.n, dtype=bool)
+        present[c["I"]] = True
+        present[c["J"]] = True
+        hit = r != RANK_UNSET
+        assert np.array_equal(hit, present)
+        k = int(hit.sum())
+        assert np.unique(r[hit]).size == k
+        assert np.array_equal(flat[r[p.order[:k]]], p.order[:k])
+        assert np.all(np.diff(r[p.order[:k]]) > 0)
+        assert np.all(np.diff(p.order[k:]) > 0)
+        # relaxed with one 'thread' is the exact scan (test_ordering.py:72-77)
+        assert np.array_equal(bb.boba_parallel(g, mode="relaxed", thread_hint=1).order, c["order"])
+
+
+def test_errors(bb):
+    with pytest.raises(ValueError):
+        bb.boba_parallel(bb.CooGraph(1, [0], [0]), mode="yolo")
+    with pytest.raises(bb.MalformedGraphError):
+        bb.apply_permutation(bb.CooGraph(3, [0], [1]), bb.Permutation.identity(2))
+    csr = bb.coo_to_csr(bb.CooGraph(3, [0], [1]))
+    with pytest.raises(ValueError):
+        bb.spmv_pull(csr, np.ones(2))
+    # the seam's narrowing keeps the reference's range check
+    from paper_2306_10410_b200 import _parallel
+
+    with pytest.raises(bb.MalformedGraphError):
+        _parallel.first_hit_chunked(np.array([0, 5]), np.array([1, 1]), 3, 4)
+
+
+def test_seam_functions(bb, medium):
+    from paper_2306_10410_b200 import _parallel as P
+
+    c = medium.case(0)
+    I, J, n = c["I"], c["J"], c["n"]
+    r, order = P.first_hit_order_sequential(I, J, n)
+    assert np.array_equal(order, c["order"]) and np.array_equal(r, c["r"])
+    assert np.array_equal(P.first_hit_chunked(I, J, n, 8), c["r"])
+    assert np.array_equal(P.first_hit_sequential(I, J, n), c["r"])
+    assert np.array_equal(P.compact_ranks(c["r"], I, J), c["order"])
+    idx, w = P.scatter_rows(c["I2"], c["J2"], None, c["offsets"])
+    assert np.array_equal(idx, c["indices"]) and w is None
+
+
+# ------------------------------------------------------------ device level
+
+@pytest.fixture(scope="module")
+def dev(bb):
+    from paper_2306_10410_b200 import device
+
+    return device
+
+
+def to_np(t):
+    return t.cpu().numpy().view(np.uint32).astype(np.int64)
+
+
+@pytest.mark.parametrize("scale,ef", [(10, 8), (14, 4), (16, 8)])
+def test_rmat_generator_matches_oracle(dev, scale, ef):
+    I, J = dev.generate_rmat(scale, ef, seed=11)
+    oI, oJ = oracle.rmat_edges(scale, ef, seed=11)
+    assert np.array_equal(to_np(I), oI) and np.array_equal(to_np(J), oJ)
+
+
+def test_grid_generator_matches_oracle(dev):
+    for rows, cols in ((1, 1), (1, 5), (4, 1), (7, 9), (64, 64)):
+        I, J = dev.generate_grid(rows, cols)
+        oI, oJ = oracle.grid_edges(rows, cols)
+        assert np.array_equal(to_np(I), oI) and np.array_equal(to_np(J), oJ)
+
+
+def pipeline_vs_oracle(dev, I, J, n, threads=8):
+    import torch
+
+    pipe = dev.Pipeline(I.numel(), n).run(I, J)
+    torch.cuda.synchronize()
+    hI, hJ = to_np(I), to_np(J)
+    order, label, I2, J2, off, idx, _ = oracle.pipeline(hI, hJ, n, threads=threads)
+    m = I.numel()
+    assert np.array_equal(to_np(pipe.order[:n]), order), "order"
+    assert np.array_equal(to_np(pipe.label[:n]), label), "label"
+    assert np.array_equal(to_np(pipe.I2[:m]), I2) and np.array_equal(to_np(pipe.J2[:m]), J2), "relabel"
+    assert np.array_equal(to_np(pipe.offsets[: n + 1]), off), "offsets"
+    assert np.array_equal(to_np(pipe.indices[:m]), idx), "indices"
+    return pipe, off, idx
+
+
+@pytest.mark.parametrize("scale,ef", [(12, 16), (18, 16), (20, 16)])
+def test_rmat_pipeline_bit_exact(dev, scale, ef):
+    import torch
+
+    I, J = dev.generate_rmat(scale, ef, seed=1)
+    n = 1 << scale
+    # randomly relabelled like the BASELINE configs (reference io.py:294-301)
+    lab = torch.from_numpy(oracle.random_labels(n, 7).astype(np.int32)).cuda()
+    I, J = dev.gather(lab, I), dev.gather(lab, J)
+    pipe, off, idx = pipeline_vs_oracle(dev, I, J, n)
+    x = np.random.default_rng(5).random(n)
+    y = dev.spmv(pipe.offsets[: n + 1], pipe.indices[: I.numel()], torch.from_numpy(x).cuda())
+    want = oracle.spmv_pull(off, idx, x)
+    np.testing.assert_allclose(y.cpu().numpy(), want, rtol=SPMV_RTOL, atol=1e-5)
+
+
+def test_grid_pipeline_bit_exact(dev):
+    import torch
+
+    I, J = dev.generate_grid(512, 512)
+    n = 512 * 512
+    lab = torch.from_numpy(oracle.random_labels(n, 7).astype(np.int32)).cuda()
+    I, J = dev.gather(lab, I), dev.gather(lab, J)
+    pipeline_vs_oracle(dev, I, J, n)
+
+
+@pytest.mark.parametrize("n", [1, 2, 255, 256, 257, 2048, 2049, 4097, (1 << 22) + 1])
+def test_radix_pass_boundaries(dev, n):
+    import torch
+
+    rng = np.random.default_rng(n)
+    m = 5003
+    I = torch.from_numpy(rng.integers(0, n, m).astype(np.int32)).cuda()
+    J = torch.from_numpy(rng.integers(0, n, m).astype(np.int32)).cuda()
+    pipeline_vs_oracle(dev, I, J, n)
+
+
+@pytest.mark.parametrize("m", [0, 1, 2, 3, 4, 5, 7, 4099])
+def test_tails_and_unaligned(dev, m):
+    import torch
+
+    rng = np.random.default_rng(m + 100)
+    n = 37
+    base = torch.from_numpy(rng.integers(0, n, 2 * m + 2).astype(np.int32)).cuda()
+    I, J = base[1: m + 1], base[m + 2: 2 * m + 2]   # 4-byte (not 16-byte) aligned views
+    if m == 0:
+        I, J = base[:0], base[:0]
+    pipeline_vs_oracle(dev, I, J, n)
+
+
+def test_stability_property_at_scale(dev):
+    """Within-row order == edge order at scale 22: carry the edge index as
+    a float64 weight; every CSR row's weights must be strictly increasing."""
+    import torch
+
+    scale = 22
+    I, J = dev.generate_rmat(scale, 16, seed=9)
+    n, m = 1 << scale, I.numel()
+    first, order, label = dev.boba_order(I, J, n)
+    I2, J2 = dev.relabel(I, J, label, n)
+    w = torch.arange(m, dtype=torch.float64, device=I.device)
+    off, idx, w_out = dev.coo_to_csr(I2, J2, n, weights=w)
+    off64 = off.to(torch.int64)
+    rows = torch.repeat_interleave(torch.arange(n, device=I.device), off64[1:] - off64[:-1])
+    e = w_out.to(torch.int64)
+    same = rows[1:] == rows[:-1]
+    assert bool(torch.all(e[1:][same] > e[:-1][same]))
+    # the moved payload is exactly the edge list sorted by row
+    assert bool(torch.all(idx == J2[e]))
+    assert bool(torch.all(rows == I2.to(torch.int64)[e]))
+    # permutation validity
+    lab = label.to(torch.int64)
+    assert bool(torch.all(torch.sort(lab).values == torch.arange(n, device=I.device)))
+    assert bool(torch.all(lab[order.to(torch.int64)] == torch.arange(n, device=I.device)))
+
+
+def test_spmv_determinism_and_integer_exactness(dev):
+    import torch
+
+    I, J = dev.generate_rmat(18, 16, seed=3)
+    n = 1 << 18
+    _, _, label = dev.boba_order(I, J, n)
+    I2, J2 = dev.relabel(I, J, label, n)
+    off, idx, _ = dev.coo_to_csr(I2, J2, n)
+    xi = torch.randint(0, 4, (n,), device=I.device).to(torch.float32)
+    y1 = dev.spmv(off, idx, xi)
+    y2 = dev.spmv(off, idx, xi)
+    assert torch.equal(y1, y2)
+    want = oracle.spmv_pull(to_np(off), to_np(idx), xi.cpu().numpy().astype(np.float64))
+    assert np.array_equal(y1.cpu().numpy().astype(np.float64), want)   # integer sums < 2^24: exact
+    xr = torch.rand(n, device=I.device)
+    assert torch.equal(dev.spmv(off, idx, xr), dev.spmv(off, idx, xr))
+
+
+def test_host_pipeline_matches_device(dev):
+    import torch
+
+    I, J = dev.generate_rmat(16, 8, seed=2)
+    n, m = 1 << 16, I.numel()
+    pipe = dev.Pipeline(m, n).run(I, J)
+    hp = dev.HostPipeline(m, n)
+    hI = I.cpu().numpy().view(np.uint32)
+    hJ = J.cpu().numpy().view(np.uint32)
+    order = np.empty(n, np.uint32)
+    label = np.empty(n, np.uint32)
+    off = np.empty(n + 1, np.uint32)
+    idx = np.empty(m, np.uint32)
+    hp.run(hI, hJ, n, order, label, off, idx)
+    torch.cuda.synchronize()
+    assert np.array_equal(order, pipe.order[:n].cpu().numpy().view(np.uint32))
+    assert np.array_equal(off, pipe.offsets[: n + 1].cpu().numpy().view(np.uint32))
+    assert np.array_equal(idx, pipe.indices[:m].cpu().numpy().view(np.uint32))
+    hp.close()

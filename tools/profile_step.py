@@ -1,0 +1,23 @@
+"""One pipeline step + one SpMV on R-MAT scale S (default 22), for ncu captures."""
+import os, sys
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle
+from paper_2306_10410_b200 import device as D
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+n, ef = 1 << scale, 16
+I, J = D.generate_rmat(scale, ef, 1)
+lab = torch.from_numpy(oracle.random_labels(n, 7).astype(np.int32)).cuda()
+I, J = D.gather(lab, I), D.gather(lab, J)
+m = I.numel()
+pipe = D.Pipeline(m, n)
+x = torch.ones(n, device="cuda")
+ws = D.spmv_workspace(n, m, "cuda")
+y = torch.empty(n, device="cuda")
+torch.cuda.synchronize()
+for _ in range(reps):
+    pipe.run(I, J)
+    D.spmv(pipe.offsets[: n + 1], pipe.indices[:m], x, out=y, ws=ws)
+torch.cuda.synchronize()
+print("done", n, m)
