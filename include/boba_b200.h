@@ -115,6 +115,14 @@ int boba_reorder_to_csr(const uint32_t *I, const uint32_t *J, const double *weig
                         uint32_t n, uint32_t *first, uint32_t *order, uint32_t *label, uint32_t *I2,
                         uint32_t *J2, uint32_t *offsets, uint32_t *indices, double *weights_out,
                         void *workspace, size_t workspace_bytes, void *stream);
+/* Same, recording events[0..4] (cudaEvent_t, entries may be NULL) on
+ * `stream` at the phase boundaries: before first occurrence, before
+ * compaction, before relabel, before COO->CSR, after COO->CSR. */
+int boba_reorder_to_csr_timed(const uint32_t *I, const uint32_t *J, const double *weights, uint64_t m,
+                              uint32_t n, uint32_t *first, uint32_t *order, uint32_t *label,
+                              uint32_t *I2, uint32_t *J2, uint32_t *offsets, uint32_t *indices,
+                              double *weights_out, void *workspace, size_t workspace_bytes,
+                              void *stream, void *const *events);
 
 /* --- Host-buffer pipeline (end to end, synchronous) ----------------------
  * A context owns device buffers for graphs up to (max_m, max_n) on the

@@ -49,6 +49,7 @@ SIGNATURES = {
     "boba_spmv": ([_P, _P, _P, _P, _P, _U32, _U64, _P, _SZ, _P], _I),
     "boba_reorder_to_csr_workspace_size": ([_U64, _U32, _I], _SZ),
     "boba_reorder_to_csr": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], _I),
+    "boba_reorder_to_csr_timed": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P], _I),
     "boba_ctx_create": ([_U64, _U32, ctypes.POINTER(_P)], _I),
     "boba_ctx_destroy": ([_P], None),
     "boba_ctx_reorder_to_csr_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P], _I),

@@ -6,6 +6,7 @@
 
 #include "../../include/boba_b200.h"
 #include "common.cuh"
+#include "hubs.cuh"
 #include "kernels.cuh"
 
 namespace {
@@ -90,7 +91,7 @@ int boba_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order,
     if (int rc = check_sizes(m, n, "boba_compact")) return rc;
     if (n == 0) return BOBA_OK;
     REQUIRE(first && order && label && ws, "boba_compact: NULL argument");
-    return cuda_status(boba::launch_compact(first, m, n, order, label, n_seen, ws, ws_bytes, num_sms(), S(stream)),
+    return cuda_status(boba::launch_compact(first, m, n, order, label, n_seen, nullptr, ws, ws_bytes, num_sms(), S(stream)),
                        "boba_compact");
 }
 
@@ -106,7 +107,7 @@ int boba_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, c
                  uint32_t* J2, uint32_t* row_counts, void* stream) {
     if (int rc = check_sizes(m, n, "boba_relabel")) return rc;
     REQUIRE((I && J && I2 && J2 && label) || m == 0, "boba_relabel: NULL argument");
-    return cuda_status(boba::launch_relabel(I, J, m, label, I2, J2, row_counts, n, num_sms(), S(stream)),
+    return cuda_status(boba::launch_relabel(I, J, m, label, nullptr, I2, J2, row_counts, n, num_sms(), S(stream)),
                        "boba_relabel");
 }
 
@@ -146,24 +147,54 @@ int boba_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, 
 size_t boba_reorder_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted) {
     size_t a = boba::compact_workspace_bytes(m, n);
     size_t b = boba::coo_to_csr_workspace_bytes(m, n, weighted != 0);
-    return align256((size_t)n * 4 + 4) + (a > b ? a : b);
+    return align256((size_t)n * 4 + 4) + align256(boba::kHubTableBytes) + (a > b ? a : b);
+}
+
+int boba_reorder_to_csr_timed(const uint32_t* I, const uint32_t* J, const double* w, uint64_t m, uint32_t n,
+                              uint32_t* first, uint32_t* order, uint32_t* label, uint32_t* I2, uint32_t* J2,
+                              uint32_t* offsets, uint32_t* indices, double* w_out, void* ws, size_t ws_bytes,
+                              void* stream, void* const* events) {
+    if (int rc = check_sizes(m, n, "boba_reorder_to_csr")) return rc;
+    REQUIRE(ws && ws_bytes >= boba_reorder_to_csr_workspace_size(m, n, w != nullptr),
+            "boba_reorder_to_csr: workspace too small");
+    REQUIRE(first && order && label && offsets, "boba_reorder_to_csr: NULL output");
+    REQUIRE((I && J && I2 && J2 && indices) || m == 0, "boba_reorder_to_csr: NULL edge arrays");
+    REQUIRE(!w || w_out || m == 0, "boba_reorder_to_csr: weights given but weights_out is NULL");
+    if (n == 0) return BOBA_OK;
+    cudaStream_t s = S(stream);
+    auto mark = [&](int i) {
+        if (events && events[i]) cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s);
+    };
+    char* base = static_cast<char*>(ws);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(base);
+    base += align256((size_t)n * 4 + 4);
+    unsigned long long* hubs = reinterpret_cast<unsigned long long*>(base);
+    base += align256(boba::kHubTableBytes);
+    void* rest = base;
+    size_t rest_bytes = ws_bytes - (size_t)(base - static_cast<char*>(ws));
+    const int sms = num_sms();
+    mark(0);
+    cudaError_t e = boba::launch_first_hit(I, J, m, n, first, false, sms, s);
+    if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: first occurrence");
+    mark(1);
+    e = boba::launch_compact(first, m, n, order, label, nullptr, hubs, rest, rest_bytes, sms, s);
+    if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: compact");
+    mark(2);
+    e = boba::launch_relabel(I, J, m, label, hubs, I2, J2, counts, n, sms, s);
+    if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: relabel");
+    mark(3);
+    e = boba::launch_coo_to_csr(I2, J2, w, m, n, counts, offsets, indices, w_out, rest, rest_bytes, sms, s);
+    if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: coo_to_csr");
+    mark(4);
+    return BOBA_OK;
 }
 
 int boba_reorder_to_csr(const uint32_t* I, const uint32_t* J, const double* w, uint64_t m, uint32_t n,
                         uint32_t* first, uint32_t* order, uint32_t* label, uint32_t* I2, uint32_t* J2,
                         uint32_t* offsets, uint32_t* indices, double* w_out, void* ws, size_t ws_bytes,
                         void* stream) {
-    if (int rc = check_sizes(m, n, "boba_reorder_to_csr")) return rc;
-    REQUIRE(ws_bytes >= boba_reorder_to_csr_workspace_size(m, n, w != nullptr),
-            "boba_reorder_to_csr: workspace too small");
-    if (n == 0) return BOBA_OK;
-    uint32_t* counts = static_cast<uint32_t*>(ws);
-    void* rest = static_cast<char*>(ws) + align256((size_t)n * 4 + 4);
-    size_t rest_bytes = ws_bytes - align256((size_t)n * 4 + 4);
-    if (int rc = boba_first_occurrence(I, J, m, n, first, 0, stream)) return rc;
-    if (int rc = boba_compact(first, m, n, order, label, nullptr, rest, rest_bytes, stream)) return rc;
-    if (int rc = boba_relabel(I, J, m, n, label, I2, J2, counts, stream)) return rc;
-    return boba_coo_to_csr(I2, J2, w, m, n, counts, offsets, indices, w_out, rest, rest_bytes, stream);
+    return boba_reorder_to_csr_timed(I, J, w, m, n, first, order, label, I2, J2, offsets, indices, w_out, ws,
+                                     ws_bytes, stream, nullptr);
 }
 
 int boba_ctx_create(uint64_t max_m, uint32_t max_n, boba_ctx** out) {

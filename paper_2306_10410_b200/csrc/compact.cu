@@ -17,6 +17,7 @@
 //                   label[v] = rank (coalesced) and order[rank] = v.
 // No gather of I||J is needed: position first[v] holds v by definition.
 #include "common.cuh"
+#include "hubs.cuh"
 #include "kernels.cuh"
 
 namespace boba {
@@ -99,7 +100,8 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
                                                     const uint32_t* __restrict__ secprefix,
                                                     const uint32_t* __restrict__ n_seen_ptr,
                                                     uint32_t* order, uint32_t* label,
-                                                    unsigned long long* status, unsigned* tile_counter) {
+                                                    unsigned long long* status, unsigned* tile_counter,
+                                                    unsigned long long* hubs) {
     __shared__ unsigned s_tile;
     __shared__ uint32_t s_scan[kScanNT / 32 + 1];
     __shared__ unsigned long long s_excl;
@@ -134,6 +136,7 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
         uint32_t r = (f[k] == BOBA_UNSET) ? iso_rank++ : rank_of(f[k], bits, secprefix);
         lab[k] = r;
         order[r] = (uint32_t)(v0 + k);
+        hub_insert(hubs, (uint32_t)(v0 + k), r);
     }
     if (v0 + kAssignVPT <= n && (reinterpret_cast<uintptr_t>(label) & 15) == 0) {
         *reinterpret_cast<uint4*>(label + v0) = make_uint4(lab[0], lab[1], lab[2], lab[3]);
@@ -177,8 +180,8 @@ CompactWs carve_compact(void* base, uint64_t m, uint32_t n) {
 size_t compact_workspace_bytes(uint64_t m, uint32_t n) { return carve_compact(nullptr, m, n).total; }
 
 cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order,
-                           uint32_t* label, uint32_t* n_seen_out, void* ws, size_t ws_bytes,
-                           int num_sms, cudaStream_t s) {
+                           uint32_t* label, uint32_t* n_seen_out, unsigned long long* hubs, void* ws,
+                           size_t ws_bytes, int num_sms, cudaStream_t s) {
     if (ws_bytes < compact_workspace_bytes(m, n)) return cudaErrorInvalidValue;
     if (n == 0) return cudaSuccess;
     const uint64_t sectors = ceil_div(2 * m, 256) + 1;
@@ -192,6 +195,10 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
     // clear bits, lookback status and counters (everything before secprefix)
     cudaError_t err = cudaMemsetAsync(ws, 0, reinterpret_cast<char*>(secprefix) - static_cast<char*>(ws), s);
     if (err != cudaSuccess) return err;
+    if (hubs) {
+        err = cudaMemsetAsync(hubs, 0xFF, kHubTableBytes, s);
+        if (err != cudaSuccess) return err;
+    }
     {
         uint64_t blocks = ceil_div(n, 256);
         uint64_t cap = (uint64_t)num_sms * 16;
@@ -200,7 +207,7 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
     k_sector_scan<<<(int)sec_tiles, kScanNT, 0, s>>>(reinterpret_cast<const uint4*>(bits), sectors,
                                                      secprefix, w.st_sec, counters + 0, n_seen);
     k_assign<<<(int)v_tiles, kScanNT, 0, s>>>(first, n, reinterpret_cast<const uint4*>(bits), secprefix,
-                                              n_seen, order, label, w.st_v, counters + 1);
+                                              n_seen, order, label, w.st_v, counters + 1, hubs);
     if (n_seen_out) cudaMemcpyAsync(n_seen_out, n_seen, 4, cudaMemcpyDeviceToDevice, s);
     return cudaGetLastError();
 }

@@ -11,11 +11,14 @@ cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, u
                              bool relaxed, int num_sms, cudaStream_t s);
 
 size_t compact_workspace_bytes(uint64_t m, uint32_t n);
+// hubs (may be NULL): kHubTableBytes table filled for phase 3 (hubs.cuh)
 cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order, uint32_t* label,
-                           uint32_t* n_seen_out, void* ws, size_t ws_bytes, int num_sms, cudaStream_t s);
+                           uint32_t* n_seen_out, unsigned long long* hubs, void* ws, size_t ws_bytes, int num_sms,
+                           cudaStream_t s);
 
-cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label, uint32_t* I2,
-                           uint32_t* J2, uint32_t* counts, uint32_t n, int num_sms, cudaStream_t s);
+cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,
+                           const unsigned long long* hubs, uint32_t* I2, uint32_t* J2, uint32_t* counts, uint32_t n,
+                           int num_sms, cudaStream_t s);
 
 cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* counts, int num_sms, cudaStream_t s);
 cudaError_t launch_row_offsets(const uint32_t* counts, uint32_t n, uint32_t* offsets, unsigned long long* status,

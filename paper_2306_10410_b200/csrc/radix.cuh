@@ -1,0 +1,229 @@
+// Stable LSD radix pass of (key, payload) uint32 pairs for COO->CSR
+// (csr.cu), in reduce-then-scan form -- no CTA ever waits on another:
+//
+//   k_radix_upsweep    per tile (TILE contiguous items) digit histogram in
+//                      shared memory -> H[d * tiles + t] (digit-major);
+//   k_scan_u32         exclusive scan of H in place (decoupled lookback over
+//                      2K-entry tiles; H is ~nb*tiles words, a few MB);
+//   k_radix_downsweep  re-reads the tile, ranks every item stably inside the
+//                      CTA and scatters it to H[d * tiles + t] + local rank,
+//                      staged through shared memory so each digit's run of
+//                      the tile is written contiguously.
+//
+// Stable in-CTA ranking: items sit in warp-striped order (warp w owns a
+// contiguous run, lane l holds items i*32 + l), so (warp, i, lane) order is
+// input order.  For each 32-item slot the peers (same digit) are found with
+// one ballot per digit bit; the lowest peer bumps the warp's 16-bit counter.
+// A per-digit scan across warps then turns warp-local ranks into tile ranks.
+#pragma once
+#include "common.cuh"
+
+namespace boba {
+
+template <int RB, int NT, int IPT>
+struct RadixCfg {
+    static constexpr int B = 1 << RB;
+    static constexpr int NW = NT / 32;
+    static constexpr int TILE = NT * IPT;
+    static constexpr int BPT = B >= NT ? B / NT : 1;              // digits per thread in the scans
+    static constexpr int HIST_BYTES = NW * B * 2;                  // 16-bit warp counters
+    static constexpr int STAGE_BYTES = TILE * 8;                   // keys + payloads
+    static constexpr int REGION = HIST_BYTES > STAGE_BYTES ? HIST_BYTES : STAGE_BYTES;
+    static constexpr size_t SMEM = (size_t)REGION + 2 * B * 4;     // + s_off, s_glob
+    static_assert(TILE < 65536, "16-bit counters and packed ranks");
+    static_assert(B % NT == 0 || NT % B == 0, "digit ownership");
+};
+
+// ------------------------------------------------------------- upsweep ---
+template <int RB, int NT, int IPT>
+__global__ void __launch_bounds__(NT) k_radix_upsweep(const uint32_t* __restrict__ keys, uint64_t m, int shift,
+                                                      int bits, uint64_t tiles, uint32_t* __restrict__ H) {
+    using C = RadixCfg<RB, NT, IPT>;
+    __shared__ uint32_t s_h[C::B];
+    const int nb = 1 << bits;
+    const uint32_t mask = (uint32_t)nb - 1u;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int d = threadIdx.x; d < nb; d += NT) s_h[d] = 0;
+        __syncthreads();
+        const uint64_t base = t * C::TILE;
+        if (base + C::TILE <= m && (C::TILE % (4 * NT)) == 0) {
+            const uint4* k4 = reinterpret_cast<const uint4*>(keys + base);
+#pragma unroll
+            for (int i = 0; i < C::TILE / (4 * NT); i++) {
+                const uint4 q = __ldg(k4 + i * NT + threadIdx.x);
+                atomicAdd(s_h + ((q.x >> shift) & mask), 1u);
+                atomicAdd(s_h + ((q.y >> shift) & mask), 1u);
+                atomicAdd(s_h + ((q.z >> shift) & mask), 1u);
+                atomicAdd(s_h + ((q.w >> shift) & mask), 1u);
+            }
+        } else {
+            for (uint64_t i = base + threadIdx.x; i < m && i < base + C::TILE; i += NT)
+                atomicAdd(s_h + ((__ldg(keys + i) >> shift) & mask), 1u);
+        }
+        __syncthreads();
+        for (int d = threadIdx.x; d < nb; d += NT) H[(uint64_t)d * tiles + t] = s_h[d];
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------- exclusive scan (u32) ---
+constexpr int kScanTileNT = 256, kScanTileIPT = 8, kScanTile = kScanTileNT * kScanTileIPT;
+
+__global__ void __launch_bounds__(kScanTileNT) k_scan_u32(uint32_t* data, uint64_t count, uint32_t add,
+                                                          unsigned long long* status, unsigned* tile_counter) {
+    __shared__ unsigned s_tile;
+    __shared__ uint32_t s_scan[kScanTileNT / 32 + 1];
+    __shared__ unsigned long long s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t i0 = tile * kScanTile + (uint64_t)threadIdx.x * kScanTileIPT;
+    uint32_t c[kScanTileIPT];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanTileIPT; k++) {
+        c[k] = (i0 + k < count) ? data[i0 + k] : 0u;
+        sum += c[k];
+    }
+    uint32_t total;
+    uint32_t ex_t = block_exclusive_sum<kScanTileNT>(sum, s_scan, &total);
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0)
+            st_volatile_u64(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | (unsigned long long)total);
+        unsigned long long ex = tile == 0 ? 0ull : warp_lookback(status, (long long)tile);
+        if (threadIdx.x == 0) {
+            if (tile != 0) st_volatile_u64(status + tile, kFlagInc | (ex + total));
+            s_excl = ex;
+        }
+    }
+    __syncthreads();
+    uint32_t run = add + (uint32_t)s_excl + ex_t;
+#pragma unroll
+    for (int k = 0; k < kScanTileIPT; k++) {
+        if (i0 + k < count) data[i0 + k] = run;
+        run += c[k];
+    }
+}
+
+// ----------------------------------------------------------- downsweep ---
+template <int RB, int NT, int IPT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __restrict__ keys_in,
+                                                              const uint32_t* __restrict__ vals_in, uint64_t m,
+                                                              int shift, int bits, uint64_t tiles,
+                                                              const uint32_t* __restrict__ H,
+                                                              uint32_t* __restrict__ keys_out,
+                                                              uint32_t* __restrict__ vals_out) {
+    using C = RadixCfg<RB, NT, IPT>;
+    constexpr int B = C::B, NW = C::NW, TILE = C::TILE, BPT = C::BPT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint16_t* s_hist = reinterpret_cast<uint16_t*>(smem_raw);            // NW x B warp counters
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(smem_raw);             // TILE (aliases s_hist later)
+    uint32_t* s_val = s_key + TILE;                                      // TILE
+    uint32_t* s_off = reinterpret_cast<uint32_t*>(smem_raw + C::REGION); // B: tile-local digit offsets
+    uint32_t* s_glob = s_off + B;                                        // B: global position - s_off
+    __shared__ uint32_t s_scan[NW + 1];
+
+    const int nb = 1 << bits;
+    const uint32_t mask = (uint32_t)nb - 1u;
+    const uint64_t tile = blockIdx.x;
+    const uint64_t tile_base = tile * TILE;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint64_t wslot = tile_base + (uint64_t)warp * 32 * IPT;
+    const bool full = tile_base + TILE <= m;
+
+    for (int i = threadIdx.x; i < NW * B / 2; i += NT) reinterpret_cast<uint32_t*>(s_hist)[i] = 0;
+    uint32_t key[IPT], rank[IPT];
+    if (full) {
+#pragma unroll
+        for (int i = 0; i < IPT; i++) key[i] = __ldg(keys_in + wslot + i * 32 + lane);
+    } else {
+#pragma unroll
+        for (int i = 0; i < IPT; i++) {
+            const uint64_t idx = wslot + (uint64_t)i * 32 + lane;
+            key[i] = idx < m ? __ldg(keys_in + idx) : 0u;
+        }
+    }
+    __syncthreads();
+    uint16_t* wh = s_hist + warp * B;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int i = 0; i < IPT; i++) {
+        const bool ok = full || wslot + (uint64_t)i * 32 + lane < m;
+        const uint32_t d = (key[i] >> shift) & mask;
+        unsigned peers = full ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, ok);
+#pragma unroll
+        for (int b = 0; b < RB; b++) {  // bits >= `bits` are zero in every lane: no effect
+            const unsigned bb = __ballot_sync(0xFFFFFFFFu, (d >> b) & 1u);
+            const unsigned t = 0u - ((d >> b) & 1u);
+            peers &= ~(bb ^ t);
+        }
+        const unsigned below = peers & lt;
+        uint32_t pre = 0;
+        if (ok) pre = wh[d];
+        __syncwarp();
+        if (ok && below == 0) wh[d] = (uint16_t)(pre + __popc(peers));
+        rank[i] = ok ? pre + __popc(below) : 0xFFFFFFFFu;
+        __syncwarp();
+    }
+    __syncthreads();
+    // Per-digit exclusive scan across warps, then across digits (tile offsets).
+    uint32_t cnt[BPT];
+#pragma unroll
+    for (int b = 0; b < BPT; b++) {
+        const int d = threadIdx.x * BPT + b;
+        uint32_t run = 0;
+        if (d < nb) {
+#pragma unroll
+            for (int w = 0; w < NW; w++) {
+                const uint32_t c = s_hist[w * B + d];
+                s_hist[w * B + d] = (uint16_t)run;
+                run += c;
+            }
+        }
+        cnt[b] = run;
+    }
+    {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int b = 0; b < BPT; b++) sum += cnt[b];
+        uint32_t tot;
+        uint32_t ex = block_exclusive_sum<NT>(sum, s_scan, &tot);
+#pragma unroll
+        for (int b = 0; b < BPT; b++) {
+            const int d = threadIdx.x * BPT + b;
+            if (d < nb) {
+                s_off[d] = ex;
+                s_glob[d] = __ldg(H + (uint64_t)d * tiles + tile) - ex;
+            }
+            ex += cnt[b];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; i++) {
+        if (rank[i] != 0xFFFFFFFFu) {
+            const uint32_t d = (key[i] >> shift) & mask;
+            rank[i] += s_off[d] + wh[d];
+        }
+    }
+    __syncthreads();  // s_hist is dead; the staging buffers alias it
+#pragma unroll
+    for (int i = 0; i < IPT; i++) {
+        if (rank[i] != 0xFFFFFFFFu) {
+            const uint64_t idx = wslot + (uint64_t)i * 32 + lane;
+            s_key[rank[i]] = key[i];
+            s_val[rank[i]] = vals_in ? __ldg(vals_in + idx) : (uint32_t)idx;  // payload read late
+        }
+    }
+    __syncthreads();
+    const uint64_t rem = m - tile_base;
+    const int items = rem < (uint64_t)TILE ? (int)rem : TILE;
+    for (int j = threadIdx.x; j < items; j += NT) {
+        const uint32_t k = s_key[j];
+        const uint32_t g = s_glob[(k >> shift) & mask] + (uint32_t)j;
+        if (keys_out) keys_out[g] = k;
+        vals_out[g] = s_val[j];
+    }
+}
+
+}  // namespace boba

@@ -3,32 +3,77 @@
 // Reference: pkg/src/boba/graph.py:280-289 apply_permutation:
 // (label[I], label[J]) with edge order (and weights) unchanged.
 //
-// One pass: 16-byte loads of I and J, eight read-only-path gathers from
-// label[] (4n bytes; L2-resident for n <= ~25M), 16-byte stores of I2 and
-// J2.  Optionally fuses the out-degree histogram of the new rows (the
-// np.bincount of graph.py:270 for the following COO->CSR) as RED.ADD.
+// One streaming pass: 16-byte loads of I and J, 16-byte stores of I2 and J2.
+// The per-endpoint cost is the random 4-byte gather label[v] (4n bytes,
+// L2-resident up to n ~ 25M) -- bounded by the L2 request rate, not HBM.
+// Two shared-memory structures cut those requests:
+//  * hub label cache: BOBA puts the hubs first, so the vertices with the
+//    smallest new labels are exactly the ones most endpoints hit.  Phase 2
+//    (k_assign) drops every vertex with label < 16K into a 16K-slot
+//    direct-mapped table (64-bit atomicMin on (label<<32 | v): the smallest
+//    label wins a slot); each CTA copies it into shared memory (128 KB) and
+//    serves hits from there.
+//  * row histogram (the np.bincount of graph.py:270 for the following
+//    COO->CSR): rows < 8K -- again the hubs -- are counted in shared memory
+//    and flushed once per CTA; other rows use RED.ADD in L2.
 #include "common.cuh"
+#include "hubs.cuh"
 #include "kernels.cuh"
 
 namespace boba {
 
-template <bool HIST>
-__global__ void __launch_bounds__(256) k_relabel(const uint4* __restrict__ I, const uint4* __restrict__ J,
-                                                 uint64_t quads, const uint32_t* __restrict__ label,
-                                                 uint4* __restrict__ I2, uint4* __restrict__ J2,
-                                                 uint32_t* counts) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += stride) {
-        uint4 a = __ldg(I + q), b = __ldg(J + q);
+constexpr int kRlNT = 1024;
+constexpr int kHubHistRows = 8192;
+
+template <bool HIST, bool HUBS>
+__global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ I, const uint4* __restrict__ J,
+                                                      uint64_t quads, const uint32_t* __restrict__ label,
+                                                      const unsigned long long* __restrict__ hubs, uint32_t n,
+                                                      uint4* __restrict__ I2, uint4* __restrict__ J2,
+                                                      uint32_t* counts) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* s_key = sm;                                    // kHubSlots
+    uint32_t* s_lab = sm + (HUBS ? (1 << kHubSlotsLog2) : 0);  // kHubSlots
+    uint32_t* s_hist = s_lab + (HUBS ? (1 << kHubSlotsLog2) : 0);  // kHubHistRows
+    if (HUBS) {
+        for (int i = threadIdx.x; i < (1 << kHubSlotsLog2); i += kRlNT) {
+            unsigned long long e = __ldg(hubs + i);
+            s_key[i] = (uint32_t)e;            // 0xFFFFFFFF when empty: never equals a vertex < n
+            s_lab[i] = (uint32_t)(e >> 32);
+        }
+    }
+    if (HIST)
+        for (int i = threadIdx.x; i < kHubHistRows; i += kRlNT) s_hist[i] = 0;
+    __syncthreads();
+    auto lookup = [&](uint32_t v) -> uint32_t {
+        if (HUBS) {
+            const uint32_t s = hub_slot(v);
+            if (s_key[s] == v) return s_lab[s];
+        }
+        return __ldg(label + v);
+    };
+    auto count = [&](uint32_t r) {
+        if (r < (uint32_t)kHubHistRows)
+            atomicAdd(s_hist + r, 1u);
+        else
+            atomicAdd(counts + r, 1u);
+    };
+    const uint64_t stride = (uint64_t)gridDim.x * kRlNT;
+    for (uint64_t q = (uint64_t)blockIdx.x * kRlNT + threadIdx.x; q < quads; q += stride) {
+        const uint4 a = __ldg(I + q), b = __ldg(J + q);
         uint4 ra, rb;
-        ra.x = __ldg(label + a.x); ra.y = __ldg(label + a.y); ra.z = __ldg(label + a.z); ra.w = __ldg(label + a.w);
-        rb.x = __ldg(label + b.x); rb.y = __ldg(label + b.y); rb.z = __ldg(label + b.z); rb.w = __ldg(label + b.w);
+        ra.x = lookup(a.x); ra.y = lookup(a.y); ra.z = lookup(a.z); ra.w = lookup(a.w);
+        rb.x = lookup(b.x); rb.y = lookup(b.y); rb.z = lookup(b.z); rb.w = lookup(b.w);
         I2[q] = ra;
         J2[q] = rb;
         if (HIST) {
-            atomicAdd(counts + ra.x, 1u); atomicAdd(counts + ra.y, 1u);
-            atomicAdd(counts + ra.z, 1u); atomicAdd(counts + ra.w, 1u);
+            count(ra.x); count(ra.y); count(ra.z); count(ra.w);
         }
+    }
+    if (HIST) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < kHubHistRows && i < (int)n; i += kRlNT)
+            if (s_hist[i]) atomicAdd(counts + i, s_hist[i]);
     }
 }
 
@@ -45,9 +90,22 @@ __global__ void k_relabel_scalar(const uint32_t* __restrict__ I, const uint32_t*
     }
 }
 
+template <bool HIST, bool HUBS>
+static void launch_vec(int grid, size_t smem, cudaStream_t s, const uint32_t* I, const uint32_t* J, uint64_t quads,
+                       const uint32_t* label, const unsigned long long* hubs, uint32_t n, uint32_t* I2, uint32_t* J2,
+                       uint32_t* counts) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_relabel<HIST, HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_relabel<HIST, HUBS><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs, n,
+                                                    (uint4*)I2, (uint4*)J2, counts);
+}
+
 cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,
-                           uint32_t* I2, uint32_t* J2, uint32_t* counts, uint32_t n, int num_sms,
-                           cudaStream_t s) {
+                           const unsigned long long* hubs, uint32_t* I2, uint32_t* J2, uint32_t* counts, uint32_t n,
+                           int num_sms, cudaStream_t s) {
     if (counts) {
         cudaError_t err = cudaMemsetAsync(counts, 0, (size_t)n * 4, s);
         if (err != cudaSuccess) return err;
@@ -56,21 +114,23 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
     const bool vec = ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(J) |
                        reinterpret_cast<uintptr_t>(I2) | reinterpret_cast<uintptr_t>(J2)) & 15) == 0;
     uint64_t done = 0;
-    const uint64_t cap = (uint64_t)num_sms * 8;
     if (vec && m >= 4) {
         const uint64_t quads = m >> 2;
-        uint64_t blocks = ceil_div(quads, 256);
-        int grid = (int)(blocks < cap ? blocks : cap);
-        if (counts)
-            k_relabel<true><<<grid, 256, 0, s>>>((const uint4*)I, (const uint4*)J, quads, label, (uint4*)I2,
-                                                 (uint4*)J2, counts);
+        uint64_t blocks = ceil_div(quads, kRlNT);
+        const int grid = (int)(blocks < (uint64_t)num_sms ? blocks : (uint64_t)num_sms);
+        const size_t smem = 4 * ((hubs ? 2 * (1 << kHubSlotsLog2) : 0) + (counts ? kHubHistRows : 0));
+        if (counts && hubs)
+            launch_vec<true, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
+        else if (counts)
+            launch_vec<true, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
+        else if (hubs)
+            launch_vec<false, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
         else
-            k_relabel<false><<<grid, 256, 0, s>>>((const uint4*)I, (const uint4*)J, quads, label, (uint4*)I2,
-                                                  (uint4*)J2, counts);
+            launch_vec<false, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
         done = quads * 4;
     }
     if (done < m) {
-        uint64_t blocks = ceil_div(m - done, 256);
+        uint64_t blocks = ceil_div(m - done, 256), cap = (uint64_t)num_sms * 8;
         int grid = (int)(blocks < cap ? blocks : cap);
         if (counts)
             k_relabel_scalar<true><<<grid, 256, 0, s>>>(I, J, done, m, label, I2, J2, counts);

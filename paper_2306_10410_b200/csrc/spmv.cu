@@ -14,16 +14,16 @@
 //     reordering shows up as L1/L2 hit rate);
 //   * each thread folds 8 items sequentially, a warp/CTA segmented scan
 //     carries partial rows across threads;
-//   * partial rows across CTAs are carried by decoupled lookback whose fold
-//     order is canonical (left to right from the CTA that started the row), so
-//     results are bitwise deterministic run to run.
+//   * a row that spans CTAs gets its partial sum from the CTA that ends it and
+//     the tails of the CTAs before it from a segmented-scan fix-up over the
+//     per-CTA tails (k_spmv_chunk_agg + k_spmv_carry); no CTA waits on another
+//     and every sum has a fixed association, so y is bitwise deterministic.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace boba {
 
 constexpr int kSpNT = 256, kSpIPT = 8, kSpTile = kSpNT * kSpIPT;
-constexpr int kSpMaxRounds = 64;
 
 struct SegVal {
     bool f;
@@ -61,37 +61,24 @@ __global__ void k_spmv_partition(const uint32_t* __restrict__ offsets, uint32_t 
     coords[b] = (uint32_t)merge_search(offsets + 1, n, 0, m, d);
 }
 
-__device__ __forceinline__ unsigned long long pack_f(unsigned long long flag, float v) {
-    return flag | (unsigned long long)__float_as_uint(v);
-}
-
+// Main pass: every row that ends inside a CTA is written here; the first row
+// a CTA ends may have started in earlier CTAs -- its partial sum is written
+// and fixed up by k_spmv_carry (no CTA ever waits on another).
 __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict__ offsets,
                                                       const uint32_t* __restrict__ indices,
                                                       const float* __restrict__ w, const float* __restrict__ x,
                                                       float* __restrict__ y, uint32_t n, uint64_t m,
                                                       const uint32_t* __restrict__ coords,
-                                                      unsigned long long* status, unsigned* tile_counter) {
+                                                      uint32_t* __restrict__ tile_head, float* __restrict__ tile_tail) {
     __shared__ uint32_t s_end[kSpTile + 1];
     __shared__ float s_val[kSpTile];
-    __shared__ uint64_t s_ij[4];
     __shared__ SegVal s_warp[kSpNT / 32];
-    __shared__ float s_chain[kSpMaxRounds * 32];
-    __shared__ float s_carry;
-    __shared__ unsigned s_tile;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
+    const uint64_t tile = blockIdx.x;
     const uint64_t total = (uint64_t)n + m;
     const uint64_t d0 = tile * kSpTile;
     const uint64_t d1 = d0 + kSpTile < total ? d0 + kSpTile : total;
-    if (threadIdx.x < 2) {
-        const uint64_t d = threadIdx.x == 0 ? d0 : d1;
-        const uint64_t i = __ldg(coords + tile + threadIdx.x);
-        s_ij[threadIdx.x * 2] = i;
-        s_ij[threadIdx.x * 2 + 1] = d - i;
-    }
-    __syncthreads();
-    const uint64_t i0 = s_ij[0], j0 = s_ij[1], i1 = s_ij[2], j1 = s_ij[3];
+    const uint64_t i0 = __ldg(coords + tile), i1 = __ldg(coords + tile + 1);
+    const uint64_t j0 = d0 - i0, j1 = d1 - i1;
     const uint32_t nrows = (uint32_t)(i1 - i0), nnz = (uint32_t)(j1 - j0);
     for (uint32_t k = threadIdx.x; k <= nrows; k += kSpNT)
         s_end[k] = (i0 + k < n) ? __ldg(offsets + i0 + 1 + k) : 0xFFFFFFFFu;
@@ -129,8 +116,7 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
     }
     // CTA segmented scan of (emitted, tail) -> exclusive carry per thread.
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    SegVal mine{emitted, acc};
-    SegVal inc = mine;
+    SegVal inc{emitted, acc};
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         SegVal up;
@@ -138,11 +124,14 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
         up.v = __shfl_up_sync(0xFFFFFFFFu, inc.v, o);
         if (lane >= (unsigned)o) inc = seg_combine(up, inc);
     }
+    SegVal lex;
+    lex.f = __shfl_up_sync(0xFFFFFFFFu, inc.f, 1);
+    lex.v = __shfl_up_sync(0xFFFFFFFFu, inc.v, 1);
+    if (lane == 0) lex = SegVal{false, 0.f};
     if (lane == 31) s_warp[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        SegVal wv = lane < kSpNT / 32 ? s_warp[lane] : SegVal{false, 0.f};
-        SegVal wi = wv;
+        SegVal wi = lane < kSpNT / 32 ? s_warp[lane] : SegVal{false, 0.f};
 #pragma unroll
         for (int o = 1; o < kSpNT / 32; o <<= 1) {
             SegVal up;
@@ -150,86 +139,116 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
             up.v = __shfl_up_sync(0xFFFFFFFFu, wi.v, o);
             if (lane >= (unsigned)o) wi = seg_combine(up, wi);
         }
-        // exclusive warp prefix
         SegVal we;
         we.f = __shfl_up_sync(0xFFFFFFFFu, wi.f, 1);
         we.v = __shfl_up_sync(0xFFFFFFFFu, wi.v, 1);
         if (lane == 0) we = SegVal{false, 0.f};
+        __syncwarp();
         if (lane < kSpNT / 32) s_warp[lane] = we;
-        // block aggregate = inclusive of the last warp
-        SegVal agg;
-        agg.f = __shfl_sync(0xFFFFFFFFu, wi.f, kSpNT / 32 - 1);
-        agg.v = __shfl_sync(0xFFFFFFFFu, wi.v, kSpNT / 32 - 1);
-        if (lane == 0) {
-            if (tile == 0)
-                st_volatile_u64(status + tile, pack_f(kFlagInc, agg.v));
-            else
-                st_volatile_u64(status + tile, pack_f(agg.f ? kFlagInc : kFlagAgg, agg.v));
+        if (lane == kSpNT / 32 - 1) {
+            tile_tail[tile] = wi.v;                    // CTA aggregate (flag = has a head row)
+            if (!wi.f) tile_head[tile] = 0xFFFFFFFFu;  // no row ends here
         }
-        // Decoupled lookback with a canonical (left-to-right) fold.
-        float carry = 0.f;
-        if (tile > 0) {
-            long long base = (long long)tile - 1;
-            int rounds = 0;
-            int stop = 0;
-            float overflow = 0.f;
-            bool overflowed = false;
-            while (true) {
-                long long idx = base - (long long)lane;
-                unsigned long long s = idx >= 0 ? ld_volatile_u64(status + idx) : kFlagInc;
-                unsigned flag = (unsigned)(s >> 62);
-                if (__any_sync(0xFFFFFFFFu, flag == 0)) continue;
-                unsigned incm = __ballot_sync(0xFFFFFFFFu, flag == 2);
-                float v = __uint_as_float((unsigned)(s & 0xFFFFFFFFull));
-                if (rounds < kSpMaxRounds) {
-                    s_chain[rounds * 32 + lane] = v;
-                } else {
-                    // pathological row spanning > 64*32 CTAs: fold this round in place
-                    overflowed = true;
-                    float r = warp_sum(incm ? ((int)lane <= __ffs(incm) - 1 ? v : 0.f) : v);
-                    overflow += r;
-                }
-                __syncwarp();
-                if (incm) {
-                    stop = __ffs(incm) - 1;
-                    break;
-                }
-                rounds++;
-                base -= 32;
-            }
-            if (lane == 0) {
-                float a;
-                int r = rounds < kSpMaxRounds ? rounds : kSpMaxRounds - 1;
-                if (!overflowed) {
-                    a = s_chain[r * 32 + stop];
-                    for (int l = stop - 1; l >= 0; l--) a += s_chain[r * 32 + l];
-                    r--;
-                } else {
-                    a = overflow;
-                }
-                for (; r >= 0; r--)
-                    for (int l = 31; l >= 0; l--) a += s_chain[r * 32 + l];
-                carry = a;
-                if (!agg.f) st_volatile_u64(status + tile, pack_f(kFlagInc, carry + agg.v));
-            }
-        }
-        if (lane == 0) s_carry = carry;
     }
     __syncthreads();
+    if (emitted) {
+        const SegVal ex = seg_combine(s_warp[warp], lex);
+        y[first_row] = first_val + ex.v;
+        if (!ex.f) tile_head[tile] = (uint32_t)first_row;  // partial: earlier CTAs add their tails
+    }
+}
+
+// Chunk aggregates of the per-CTA (has_head, tail) pairs: a segmented sum
+// over kSpChunk consecutive CTAs, one thread per CTA.
+constexpr int kSpChunk = 1024;
+
+__device__ __forceinline__ SegVal block_seg_scan(SegVal v, SegVal* s_w, SegVal* total, SegVal* excl) {
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    SegVal inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        SegVal up;
+        up.f = __shfl_up_sync(0xFFFFFFFFu, inc.f, o);
+        up.v = __shfl_up_sync(0xFFFFFFFFu, inc.v, o);
+        if (lane >= (unsigned)o) inc = seg_combine(up, inc);
+    }
     SegVal lex;
     lex.f = __shfl_up_sync(0xFFFFFFFFu, inc.f, 1);
     lex.v = __shfl_up_sync(0xFFFFFFFFu, inc.v, 1);
     if (lane == 0) lex = SegVal{false, 0.f};
-    if (emitted) {
-        SegVal ex = seg_combine(s_warp[warp], lex);
-        float c = ex.f ? ex.v : s_carry + ex.v;
-        y[first_row] = first_val + c;
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        SegVal wi = s_w[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            SegVal up;
+            up.f = __shfl_up_sync(0xFFFFFFFFu, wi.f, o);
+            up.v = __shfl_up_sync(0xFFFFFFFFu, wi.v, o);
+            if (lane >= (unsigned)o) wi = seg_combine(up, wi);
+        }
+        SegVal we;
+        we.f = __shfl_up_sync(0xFFFFFFFFu, wi.f, 1);
+        we.v = __shfl_up_sync(0xFFFFFFFFu, wi.v, 1);
+        if (lane == 0) we = SegVal{false, 0.f};
+        __syncwarp();
+        s_w[lane] = we;
+        if (lane == 31) s_w[32] = wi;
+    }
+    __syncthreads();
+    *excl = seg_combine(s_w[warp], lex);
+    *total = s_w[32];
+    return inc;
+}
+
+__global__ void __launch_bounds__(kSpChunk) k_spmv_chunk_agg(const uint32_t* __restrict__ tile_head,
+                                                             const float* __restrict__ tile_tail, uint64_t tiles,
+                                                             unsigned* chunk_flag, float* chunk_val) {
+    __shared__ SegVal s_w[33];
+    const uint64_t t = (uint64_t)blockIdx.x * kSpChunk + threadIdx.x;
+    SegVal v = t < tiles ? SegVal{tile_head[t] != 0xFFFFFFFFu, tile_tail[t]} : SegVal{false, 0.f};
+    SegVal total, excl;
+    block_seg_scan(v, s_w, &total, &excl);
+    if (threadIdx.x == 0) {
+        chunk_flag[blockIdx.x] = total.f;
+        chunk_val[blockIdx.x] = total.v;
+    }
+}
+
+// y[head row of CTA t] += (segmented sum of the tails of the CTAs before t
+// back to the last one that ended a row) -- fixed association, so the SpMV
+// is bitwise deterministic.
+__global__ void __launch_bounds__(kSpChunk) k_spmv_carry(const uint32_t* __restrict__ tile_head,
+                                                         const float* __restrict__ tile_tail, uint64_t tiles,
+                                                         const unsigned* __restrict__ chunk_flag,
+                                                         const float* __restrict__ chunk_val, float* y) {
+    __shared__ SegVal s_w[33];
+    __shared__ float s_cin;
+    if (threadIdx.x == 0) {
+        // carry into this chunk: fold chunk aggregates left to right from the
+        // last chunk that ended a row (normally just the previous chunk)
+        long long c = (long long)blockIdx.x - 1;
+        while (c > 0 && !chunk_flag[c]) c--;
+        float a = 0.f;
+        for (long long k = c < 0 ? 0 : c; k < (long long)blockIdx.x; k++) a += chunk_val[k];
+        s_cin = blockIdx.x == 0 ? 0.f : a;
+    }
+    __syncthreads();
+    const uint64_t t = (uint64_t)blockIdx.x * kSpChunk + threadIdx.x;
+    const uint32_t head = t < tiles ? tile_head[t] : 0xFFFFFFFFu;
+    SegVal v = t < tiles ? SegVal{head != 0xFFFFFFFFu, tile_tail[t]} : SegVal{false, 0.f};
+    SegVal total, excl;
+    block_seg_scan(v, s_w, &total, &excl);
+    if (head != 0xFFFFFFFFu && t > 0) {
+        const float carry = excl.f ? excl.v : s_cin + excl.v;
+        y[head] += carry;
     }
 }
 
 size_t spmv_workspace_bytes(uint32_t n, uint64_t m) {
     const uint64_t tiles = ceil_div((uint64_t)n + m, kSpTile);
-    return ((tiles + 1) * 8 + 64 + 255) / 256 * 256 + (tiles + 2) * 4;
+    const uint64_t chunks = ceil_div(tiles, kSpChunk);
+    return ((tiles + 2) * 4 + 255) / 256 * 256 * 3 + ((chunks + 1) * 8 + 255) / 256 * 256;
 }
 
 cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,
@@ -237,14 +256,20 @@ cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const 
     if (n == 0) return cudaSuccess;
     if (ws_bytes < spmv_workspace_bytes(n, m)) return cudaErrorInvalidValue;
     const uint64_t tiles = ceil_div((uint64_t)n + m, kSpTile);
-    unsigned long long* status = static_cast<unsigned long long*>(ws);
-    unsigned* counter = reinterpret_cast<unsigned*>(status + tiles + 1);
-    const size_t head = ((tiles + 1) * 8 + 64 + 255) / 256 * 256;
-    uint32_t* coords = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + head);
-    cudaError_t e = cudaMemsetAsync(ws, 0, head, s);
-    if (e != cudaSuccess) return e;
+    const uint64_t chunks = ceil_div(tiles, kSpChunk);
+    const size_t arr = ((tiles + 2) * 4 + 255) / 256 * 256;
+    char* p = static_cast<char*>(ws);
+    uint32_t* coords = reinterpret_cast<uint32_t*>(p);
+    uint32_t* tile_head = reinterpret_cast<uint32_t*>(p + arr);
+    float* tile_tail = reinterpret_cast<float*>(p + 2 * arr);
+    unsigned* chunk_flag = reinterpret_cast<unsigned*>(p + 3 * arr);
+    float* chunk_val = reinterpret_cast<float*>(chunk_flag + chunks);
     k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
-    k_spmv_merge<<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, status, counter);
+    k_spmv_merge<<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail);
+    if (tiles > 1) {
+        k_spmv_chunk_agg<<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val);
+        k_spmv_carry<<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val, y);
+    }
     return cudaGetLastError();
 }
 
