@@ -111,6 +111,32 @@ __device__ __forceinline__ unsigned long long warp_lookback(const unsigned long 
     return excl;
 }
 
+// Same protocol, combining with min instead of +: returns the min of the
+// values of all tiles before `tile` (kValMask if none).
+__device__ __forceinline__ unsigned long long warp_lookback_min(const unsigned long long* status, long long tile) {
+    const unsigned lane = lane_id();
+    unsigned long long acc = kValMask;
+    long long base = tile - 1;
+    while (base >= 0) {
+        long long idx = base - (long long)lane;
+        unsigned long long s = idx >= 0 ? ld_volatile_u64(status + idx) : (kFlagInc | kValMask);
+        unsigned flag = (unsigned)(s >> 62);
+        if (__any_sync(0xFFFFFFFFu, flag == 0)) continue;
+        unsigned inc = __ballot_sync(0xFFFFFFFFu, flag == 2);
+        int stop = inc ? __ffs(inc) - 1 : 31;
+        unsigned long long v = ((int)lane <= stop) ? (s & kValMask) : kValMask;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long u = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+            v = u < v ? u : v;
+        }
+        acc = v < acc ? v : acc;
+        if (inc) break;
+        base -= 32;
+    }
+    return acc;
+}
+
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 }  // namespace boba

@@ -70,6 +70,86 @@ __global__ void __launch_bounds__(kOffNT) k_scan_offsets(const uint32_t* __restr
     }
 }
 
+// ------------------------------------------- offsets from sorted rows ---
+// Without a row histogram: after the last radix pass the rows are sorted, so
+// offsets[key[g]] = g wherever the key changes (offsets pre-filled with
+// 0xFFFFFFFF, offsets[n] = m), then a suffix-min scan gives every empty row
+// the start of the next non-empty one.
+__global__ void k_row_starts(const uint32_t* __restrict__ keys, uint64_t m, uint32_t n, uint32_t* offsets) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < m; g += stride) {
+        const uint32_t k = __ldg(keys + g);
+        if (g == 0 || __ldg(keys + g - 1) != k) offsets[k] = (uint32_t)g;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) offsets[n] = (uint32_t)m;
+}
+
+constexpr int kSmNT = 256, kSmIPT = 8, kSmTile = kSmNT * kSmIPT;
+
+// In-place suffix minimum over data[0..count): tiles are taken from the end.
+__global__ void __launch_bounds__(kSmNT) k_suffix_min(uint32_t* data, uint64_t count, unsigned long long* status,
+                                                      unsigned* tile_counter) {
+    __shared__ unsigned s_tile;
+    __shared__ uint32_t s_w[kSmNT / 32];
+    __shared__ unsigned long long s_carry;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t hi = count - tile * kSmTile;               // exclusive end of this tile
+    const long long lo_t = (long long)hi - kSmTile;
+    // thread t owns elements [hi - (t+1)*IPT, hi - t*IPT), scanned from the top
+    uint32_t v[kSmIPT];
+    uint32_t run = 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < kSmIPT; k++) {
+        const long long i = (long long)hi - 1 - (long long)threadIdx.x * kSmIPT - k;
+        v[k] = (i >= 0 && i >= lo_t) ? data[i] : 0xFFFFFFFFu;
+        run = v[k] < run ? v[k] : run;
+    }
+    // exclusive suffix-min across threads (thread 0 is the top of the tile)
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= (unsigned)o) inc = u < inc ? u : inc;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint32_t wv = lane < kSmNT / 32 ? s_w[lane] : 0xFFFFFFFFu;
+        uint32_t wi = wv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t u = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= (unsigned)o) wi = u < wi ? u : wi;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, wi, kSmNT / 32 - 1);
+        const uint32_t wex = __shfl_up_sync(0xFFFFFFFFu, wi, 1);
+        if (lane < kSmNT / 32) s_w[lane] = lane == 0 ? 0xFFFFFFFFu : wex;
+        if (lane == 0)
+            st_volatile_u64(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | (unsigned long long)total);
+        unsigned long long c = tile == 0 ? kValMask : warp_lookback_min(status, (long long)tile);
+        if (lane == 0) {
+            const unsigned long long t64 = total;
+            if (tile != 0) st_volatile_u64(status + tile, kFlagInc | (c < t64 ? c : t64));
+            s_carry = c;
+        }
+    }
+    __syncthreads();
+    uint32_t ex = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+    if (lane == 0) ex = 0xFFFFFFFFu;
+    ex = s_w[warp] < ex ? s_w[warp] : ex;
+    const unsigned long long c = s_carry;
+    uint32_t acc = c < (unsigned long long)ex ? (uint32_t)c : ex;
+#pragma unroll
+    for (int k = 0; k < kSmIPT; k++) {
+        const long long i = (long long)hi - 1 - (long long)threadIdx.x * kSmIPT - k;
+        acc = v[k] < acc ? v[k] : acc;
+        if (i >= 0 && i >= lo_t) data[i] = acc;
+    }
+}
+
 }  // namespace boba
 
 #include "radix.cuh"
@@ -159,7 +239,7 @@ CsrWs carve(void* base, uint64_t m, uint32_t n) {
     const uint64_t hcount = tiles * (uint64_t)maxnb;
     w.H = (uint32_t*)take(hcount * 4 + 16);
     w.scan_status = (unsigned long long*)take((ceil_div(hcount, kScanTile) + 1) * 8);
-    w.off_status = (unsigned long long*)take((ceil_div((uint64_t)n + 1, kOffTile) + 1) * 8);
+    w.off_status = (unsigned long long*)take((ceil_div((uint64_t)n + 1, kOffTile) + ceil_div((uint64_t)n + 1, kSmTile) + 2) * 8);
     w.counters = (unsigned*)take(64);
     w.total = off;
     return w;
@@ -231,19 +311,23 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
     const bool weighted = w != nullptr;
     CsrWs W = carve(ws, m, n);
     if (ws_bytes < W.total) return cudaErrorInvalidValue;
-    cudaError_t e;
-    const uint32_t* counts = counts_in;
-    if (!counts) {
-        e = launch_hist(I2, m, n, W.counts, num_sms, s);
-        if (e != cudaSuccess) return e;
-        counts = W.counts;
+    cudaError_t e = cudaSuccess;
+    if (counts_in) {
+        // caller supplied the row histogram: offsets = exclusive scan of it
+        e = launch_row_offsets(counts_in, n, offsets, W.off_status, W.counters + 1, s);
+    } else if (m == 0) {
+        e = cudaMemsetAsync(offsets, 0, ((size_t)n + 1) * 4, s);
     }
-    e = launch_row_offsets(counts, n, offsets, W.off_status, W.counters + 1, s);
     if (e != cudaSuccess || m == 0) return e;
     const CsrPlan p = plan_for(n);
     if (p.passes == 0) {
         // n == 1: every edge is in row 0; the stable order is the edge order.
-        e = cudaMemcpyAsync(indices, J2, m * 4, cudaMemcpyDeviceToDevice, s);
+        if (!counts_in) {
+            const uint32_t h[2] = {0u, (uint32_t)m};
+            e = cudaMemcpyAsync(offsets, h, 8, cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // h lives on this stack frame
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(indices, J2, m * 4, cudaMemcpyDeviceToDevice, s);
         if (e == cudaSuccess && weighted) e = cudaMemcpyAsync(w_out, w, m * 8, cudaMemcpyDeviceToDevice, s);
         return e;
     }
@@ -252,13 +336,27 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
     for (int i = 0; i < p.passes; i++) {
         const bool last = i == p.passes - 1;
         // pass i writes bufs[2(i&1)], bufs[2(i&1)+1]; it reads the other parity.
-        uint32_t* kout = last ? nullptr : W.bufs[(i & 1) * 2];
+        // The last pass keeps the sorted rows only when offsets come from them.
+        uint32_t* kout = (last && counts_in) ? nullptr : W.bufs[(i & 1) * 2];
         uint32_t* vout = (last && !weighted) ? indices : W.bufs[(i & 1) * 2 + 1];
         e = dispatch_pass(p.v, kin, vin, m, p.shift[i], p.bits[i], W.H, W.scan_status, W.counters, kout, vout,
                           num_sms, s);
         if (e != cudaSuccess) return e;
         kin = kout;
         vin = vout;
+    }
+    if (!counts_in) {
+        // kin = rows in CSR order
+        e = cudaMemsetAsync(offsets, 0xFF, ((size_t)n + 1) * 4, s);
+        if (e != cudaSuccess) return e;
+        const uint64_t blocks = ceil_div(m, 256), cap = (uint64_t)num_sms * 8;
+        k_row_starts<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(kin, m, n, offsets);
+        const uint64_t sm_tiles = ceil_div((uint64_t)n + 1, kSmTile);
+        unsigned long long* sm_status = W.off_status + ceil_div((uint64_t)n + 1, kOffTile) + 1;
+        e = cudaMemsetAsync(sm_status, 0, sm_tiles * 8, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(W.counters + 2, 0, 4, s);
+        if (e != cudaSuccess) return e;
+        k_suffix_min<<<(unsigned)sm_tiles, kSmNT, 0, s>>>(offsets, (uint64_t)n + 1, sm_status, W.counters + 2);
     }
     if (weighted) {
         const uint64_t blocks = ceil_div(m, 256), cap = (uint64_t)num_sms * 8;
