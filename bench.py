@@ -74,7 +74,7 @@ def peaks():
 class ClockSampler:
     """Samples SM clock and throttle reasons with NVML while running."""
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=0.005):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self.max_mhz = None
@@ -390,7 +390,6 @@ def run_ours(args):
                "note": "oracle/boba_oracle.c (reference restated in C); first-hit on all cores, "
                        "rest single-threaded as in the reference"}
 
-    launches_per_step = 1 + (1 if m & 3 else 0) + 3 + 1 + (1 + 3 * csr_passes(n))  # first-hit, mark/scan/assign, relabel, offsets + per pass (digit hist, base, onesweep)
     line = {
         "metric": "BOBA reorder+COO->CSR GEdges/s",
         "value": round(value, 3),
@@ -411,7 +410,7 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "spmv": spmv_info,
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches_per_step(m, n) * args.steps,
         "clocks": clk.summary(),
     }
     if rank == 0:
@@ -422,8 +421,16 @@ def run_ours(args):
 
 def csr_passes(n):
     bits = 0 if n <= 1 else (n - 1).bit_length()
-    maxb = 11 if os.environ.get("BOBA_RADIX_MAX_BITS", "8") == "11" else 8
+    maxb = 11 if os.environ.get("BOBA_RADIX_CFG", "a").startswith("1") else 8
     return 0 if bits == 0 else -(-bits // maxb)
+
+
+def launches_per_step(m, n):
+    """Kernels boba_reorder_to_csr launches (csrc/api.cu): first occurrence
+    (+ scalar tail), mark/sector-scan/assign, relabel (+ scalar tail), and per
+    radix pass upsweep/scan/downsweep, then row starts + suffix-min."""
+    tail = 1 if m % 4 else 0
+    return (1 + tail) + 3 + (1 + tail) + 3 * csr_passes(n) + 2
 
 
 def main():

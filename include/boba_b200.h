@@ -107,6 +107,11 @@ size_t boba_spmv_workspace_size(uint32_t n, uint64_t m);
 int boba_spmv(const uint32_t *offsets, const uint32_t *indices, const float *weights,
               const float *x, float *y, uint32_t n, uint64_t m, void *workspace,
               size_t workspace_bytes, void *stream);
+/* Same in float64 -- the reference's own precision (kernels.py:30-52); the
+ * drop-in spmv_pull uses it.  Same workspace size. */
+int boba_spmv_f64(const uint32_t *offsets, const uint32_t *indices, const double *weights,
+                  const double *x, double *y, uint32_t n, uint64_t m, void *workspace,
+                  size_t workspace_bytes, void *stream);
 
 /* --- Fused device pipeline (reference bench.py:135-149: reorder = BOBA +
  * apply_permutation, convert = coo_to_csr) ------------------------------ */

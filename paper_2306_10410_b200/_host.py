@@ -97,7 +97,7 @@ def spmv(offsets, indices, x, weights=None) -> np.ndarray:
     m = int(np.asarray(indices).size)
     do = to_device_ids(offsets, m + 1, "offsets")
     di = to_device_ids(indices, max(n, 1), "indices") if m else torch.empty(0, dtype=D.ID, device=dev)
-    dx = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
-    dw = None if weights is None else torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float32)).to(dev)
-    y = D.spmv(do, di, dx, dw)
-    return y.cpu().numpy().astype(np.float64)
+    # float64 like the reference (kernels.py:30-52); device.spmv also offers fp32
+    dx = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+    dw = None if weights is None else torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
+    return D.spmv(do, di, dx, dw).cpu().numpy()

@@ -144,6 +144,15 @@ int boba_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, 
     return cuda_status(boba::launch_spmv(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream)), "boba_spmv");
 }
 
+int boba_spmv_f64(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x, double* y,
+                  uint32_t n, uint64_t m, void* ws, size_t ws_bytes, void* stream) {
+    if (n == 0) return BOBA_OK;
+    REQUIRE(offsets && x && y && ws && (indices || m == 0), "boba_spmv_f64: NULL argument");
+    REQUIRE((uint64_t)n + m < 0xFFFFFFFFull * 2048ull, "boba_spmv_f64: too large");
+    return cuda_status(boba::launch_spmv_f64(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream)),
+                       "boba_spmv_f64");
+}
+
 size_t boba_reorder_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted) {
     size_t a = boba::compact_workspace_bytes(m, n);
     size_t b = boba::coo_to_csr_workspace_bytes(m, n, weighted != 0);

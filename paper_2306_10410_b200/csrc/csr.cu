@@ -77,7 +77,19 @@ __global__ void __launch_bounds__(kOffNT) k_scan_offsets(const uint32_t* __restr
 // the start of the next non-empty one.
 __global__ void k_row_starts(const uint32_t* __restrict__ keys, uint64_t m, uint32_t n, uint32_t* offsets) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < m; g += stride) {
+    const uint64_t quads = m >> 2;
+    const bool vec = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+    const uint64_t vq = vec ? quads : 0;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < vq; q += stride) {
+        const uint4 k = __ldg(reinterpret_cast<const uint4*>(keys) + q);
+        const uint64_t g = 4 * q;
+        const uint32_t p = g ? __ldg(keys + g - 1) : ~k.x;
+        if (p != k.x) offsets[k.x] = (uint32_t)g;
+        if (k.x != k.y) offsets[k.y] = (uint32_t)(g + 1);
+        if (k.y != k.z) offsets[k.z] = (uint32_t)(g + 2);
+        if (k.z != k.w) offsets[k.w] = (uint32_t)(g + 3);
+    }
+    for (uint64_t g = 4 * vq + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < m; g += stride) {
         const uint32_t k = __ldg(keys + g);
         if (g == 0 || __ldg(keys + g - 1) != k) offsets[k] = (uint32_t)g;
     }
@@ -349,7 +361,7 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
         // kin = rows in CSR order
         e = cudaMemsetAsync(offsets, 0xFF, ((size_t)n + 1) * 4, s);
         if (e != cudaSuccess) return e;
-        const uint64_t blocks = ceil_div(m, 256), cap = (uint64_t)num_sms * 8;
+        const uint64_t blocks = ceil_div(ceil_div(m, 4), 256), cap = (uint64_t)num_sms * 16;
         k_row_starts<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(kin, m, n, offsets);
         const uint64_t sm_tiles = ceil_div((uint64_t)n + 1, kSmTile);
         unsigned long long* sm_status = W.off_status + ceil_div((uint64_t)n + 1, kOffTile) + 1;

@@ -1,4 +1,6 @@
-// Phase 5 -- CSR SpMV, fp32: y[v] = sum_{k in row v} w[k] * x[indices[k]].
+// Phase 5 -- CSR SpMV: y[v] = sum_{k in row v} w[k] * x[indices[k]], in fp32
+// (the benchmarked path, north star) or fp64 (the reference's precision, used
+// by the drop-in spmv_pull).
 //
 // Reference: pkg/src/boba/kernels.py:30-52 spmv_pull (x[indices] gather,
 // optional weights, per-row sums with empty rows = 0; kernels.py:19-27).
@@ -25,13 +27,15 @@ namespace boba {
 
 constexpr int kSpNT = 256, kSpIPT = 8, kSpTile = kSpNT * kSpIPT;
 
-struct SegVal {
+template <typename T>
+struct SegValT {
     bool f;
-    float v;
+    T v;
 };
 
-__device__ __forceinline__ SegVal seg_combine(SegVal a, SegVal b) {
-    return b.f ? b : SegVal{a.f, a.v + b.v};
+template <typename T>
+__device__ __forceinline__ SegValT<T> seg_combine(SegValT<T> a, SegValT<T> b) {
+    return b.f ? b : SegValT<T>{a.f, a.v + b.v};
 }
 
 // Merge-path search: number of row ends consumed at diagonal `diag` when
@@ -64,14 +68,16 @@ __global__ void k_spmv_partition(const uint32_t* __restrict__ offsets, uint32_t 
 // Main pass: every row that ends inside a CTA is written here; the first row
 // a CTA ends may have started in earlier CTAs -- its partial sum is written
 // and fixed up by k_spmv_carry (no CTA ever waits on another).
+template <typename T>
 __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict__ offsets,
                                                       const uint32_t* __restrict__ indices,
-                                                      const float* __restrict__ w, const float* __restrict__ x,
-                                                      float* __restrict__ y, uint32_t n, uint64_t m,
+                                                      const T* __restrict__ w, const T* __restrict__ x,
+                                                      T* __restrict__ y, uint32_t n, uint64_t m,
                                                       const uint32_t* __restrict__ coords,
-                                                      uint32_t* __restrict__ tile_head, float* __restrict__ tile_tail) {
+                                                      uint32_t* __restrict__ tile_head, T* __restrict__ tile_tail) {
+    using SegVal = SegValT<T>;
     __shared__ uint32_t s_end[kSpTile + 1];
-    __shared__ float s_val[kSpTile];
+    __shared__ T s_val[kSpTile];
     __shared__ SegVal s_warp[kSpNT / 32];
     const uint64_t tile = blockIdx.x;
     const uint64_t total = (uint64_t)n + m;
@@ -83,7 +89,7 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
     for (uint32_t k = threadIdx.x; k <= nrows; k += kSpNT)
         s_end[k] = (i0 + k < n) ? __ldg(offsets + i0 + 1 + k) : 0xFFFFFFFFu;
     for (uint32_t k = threadIdx.x; k < nnz; k += kSpNT) {
-        float p = __ldg(x + __ldg(indices + j0 + k));
+        T p = __ldg(x + __ldg(indices + j0 + k));
         if (w) p *= __ldg(w + j0 + k);
         s_val[k] = p;
     }
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
     uint32_t it = (uint32_t)merge_search(s_end, nrows, j0, nnz, diag);
     uint32_t jt = diag - it;
     const uint32_t items = items_tile - diag < (uint32_t)kSpIPT ? items_tile - diag : (uint32_t)kSpIPT;
-    float acc = 0.f, first_val = 0.f;
+    T acc = 0, first_val = 0;
     uint64_t first_row = 0;
     bool emitted = false;
     for (uint32_t k = 0; k < items; k++) {
@@ -110,7 +116,7 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
             } else {
                 y[row] = acc;
             }
-            acc = 0.f;
+            acc = 0;
             it++;
         }
     }
@@ -127,11 +133,11 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
     SegVal lex;
     lex.f = __shfl_up_sync(0xFFFFFFFFu, inc.f, 1);
     lex.v = __shfl_up_sync(0xFFFFFFFFu, inc.v, 1);
-    if (lane == 0) lex = SegVal{false, 0.f};
+    if (lane == 0) lex = SegVal{false, T(0)};
     if (lane == 31) s_warp[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        SegVal wi = lane < kSpNT / 32 ? s_warp[lane] : SegVal{false, 0.f};
+        SegVal wi = lane < kSpNT / 32 ? s_warp[lane] : SegVal{false, T(0)};
 #pragma unroll
         for (int o = 1; o < kSpNT / 32; o <<= 1) {
             SegVal up;
@@ -142,7 +148,7 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
         SegVal we;
         we.f = __shfl_up_sync(0xFFFFFFFFu, wi.f, 1);
         we.v = __shfl_up_sync(0xFFFFFFFFu, wi.v, 1);
-        if (lane == 0) we = SegVal{false, 0.f};
+        if (lane == 0) we = SegVal{false, T(0)};
         __syncwarp();
         if (lane < kSpNT / 32) s_warp[lane] = we;
         if (lane == kSpNT / 32 - 1) {
@@ -162,7 +168,10 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
 // over kSpChunk consecutive CTAs, one thread per CTA.
 constexpr int kSpChunk = 1024;
 
-__device__ __forceinline__ SegVal block_seg_scan(SegVal v, SegVal* s_w, SegVal* total, SegVal* excl) {
+template <typename T>
+__device__ __forceinline__ SegValT<T> block_seg_scan(SegValT<T> v, SegValT<T>* s_w, SegValT<T>* total,
+                                                     SegValT<T>* excl) {
+    using SegVal = SegValT<T>;
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     SegVal inc = v;
 #pragma unroll
@@ -175,7 +184,7 @@ __device__ __forceinline__ SegVal block_seg_scan(SegVal v, SegVal* s_w, SegVal* 
     SegVal lex;
     lex.f = __shfl_up_sync(0xFFFFFFFFu, inc.f, 1);
     lex.v = __shfl_up_sync(0xFFFFFFFFu, inc.v, 1);
-    if (lane == 0) lex = SegVal{false, 0.f};
+    if (lane == 0) lex = SegVal{false, T(0)};
     if (lane == 31) s_w[warp] = inc;
     __syncthreads();
     if (warp == 0) {
@@ -190,7 +199,7 @@ __device__ __forceinline__ SegVal block_seg_scan(SegVal v, SegVal* s_w, SegVal* 
         SegVal we;
         we.f = __shfl_up_sync(0xFFFFFFFFu, wi.f, 1);
         we.v = __shfl_up_sync(0xFFFFFFFFu, wi.v, 1);
-        if (lane == 0) we = SegVal{false, 0.f};
+        if (lane == 0) we = SegVal{false, T(0)};
         __syncwarp();
         s_w[lane] = we;
         if (lane == 31) s_w[32] = wi;
@@ -201,14 +210,16 @@ __device__ __forceinline__ SegVal block_seg_scan(SegVal v, SegVal* s_w, SegVal* 
     return inc;
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kSpChunk) k_spmv_chunk_agg(const uint32_t* __restrict__ tile_head,
-                                                             const float* __restrict__ tile_tail, uint64_t tiles,
-                                                             unsigned* chunk_flag, float* chunk_val) {
+                                                             const T* __restrict__ tile_tail, uint64_t tiles,
+                                                             unsigned* chunk_flag, T* chunk_val) {
+    using SegVal = SegValT<T>;
     __shared__ SegVal s_w[33];
     const uint64_t t = (uint64_t)blockIdx.x * kSpChunk + threadIdx.x;
-    SegVal v = t < tiles ? SegVal{tile_head[t] != 0xFFFFFFFFu, tile_tail[t]} : SegVal{false, 0.f};
+    SegVal v = t < tiles ? SegVal{tile_head[t] != 0xFFFFFFFFu, tile_tail[t]} : SegVal{false, T(0)};
     SegVal total, excl;
-    block_seg_scan(v, s_w, &total, &excl);
+    block_seg_scan<T>(v, s_w, &total, &excl);
     if (threadIdx.x == 0) {
         chunk_flag[blockIdx.x] = total.f;
         chunk_val[blockIdx.x] = total.v;
@@ -218,29 +229,31 @@ __global__ void __launch_bounds__(kSpChunk) k_spmv_chunk_agg(const uint32_t* __r
 // y[head row of CTA t] += (segmented sum of the tails of the CTAs before t
 // back to the last one that ended a row) -- fixed association, so the SpMV
 // is bitwise deterministic.
+template <typename T>
 __global__ void __launch_bounds__(kSpChunk) k_spmv_carry(const uint32_t* __restrict__ tile_head,
-                                                         const float* __restrict__ tile_tail, uint64_t tiles,
+                                                         const T* __restrict__ tile_tail, uint64_t tiles,
                                                          const unsigned* __restrict__ chunk_flag,
-                                                         const float* __restrict__ chunk_val, float* y) {
+                                                         const T* __restrict__ chunk_val, T* y) {
+    using SegVal = SegValT<T>;
     __shared__ SegVal s_w[33];
-    __shared__ float s_cin;
+    __shared__ T s_cin;
     if (threadIdx.x == 0) {
         // carry into this chunk: fold chunk aggregates left to right from the
         // last chunk that ended a row (normally just the previous chunk)
         long long c = (long long)blockIdx.x - 1;
         while (c > 0 && !chunk_flag[c]) c--;
-        float a = 0.f;
+        T a = 0;
         for (long long k = c < 0 ? 0 : c; k < (long long)blockIdx.x; k++) a += chunk_val[k];
-        s_cin = blockIdx.x == 0 ? 0.f : a;
+        s_cin = blockIdx.x == 0 ? T(0) : a;
     }
     __syncthreads();
     const uint64_t t = (uint64_t)blockIdx.x * kSpChunk + threadIdx.x;
     const uint32_t head = t < tiles ? tile_head[t] : 0xFFFFFFFFu;
-    SegVal v = t < tiles ? SegVal{head != 0xFFFFFFFFu, tile_tail[t]} : SegVal{false, 0.f};
+    SegVal v = t < tiles ? SegVal{head != 0xFFFFFFFFu, tile_tail[t]} : SegVal{false, T(0)};
     SegVal total, excl;
-    block_seg_scan(v, s_w, &total, &excl);
+    block_seg_scan<T>(v, s_w, &total, &excl);
     if (head != 0xFFFFFFFFu && t > 0) {
-        const float carry = excl.f ? excl.v : s_cin + excl.v;
+        const T carry = excl.f ? excl.v : s_cin + excl.v;
         y[head] += carry;
     }
 }
@@ -248,29 +261,41 @@ __global__ void __launch_bounds__(kSpChunk) k_spmv_carry(const uint32_t* __restr
 size_t spmv_workspace_bytes(uint32_t n, uint64_t m) {
     const uint64_t tiles = ceil_div((uint64_t)n + m, kSpTile);
     const uint64_t chunks = ceil_div(tiles, kSpChunk);
-    return ((tiles + 2) * 4 + 255) / 256 * 256 * 3 + ((chunks + 1) * 8 + 255) / 256 * 256;
+    const size_t arr = ((tiles + 2) * 8 + 255) / 256 * 256;   // sized for double
+    return arr * 3 + ((chunks + 1) * 16 + 255) / 256 * 256;
 }
 
-cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,
-                        uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s) {
+template <typename T>
+cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, const T* w, const T* x, T* y, uint32_t n,
+                          uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     if (ws_bytes < spmv_workspace_bytes(n, m)) return cudaErrorInvalidValue;
     const uint64_t tiles = ceil_div((uint64_t)n + m, kSpTile);
     const uint64_t chunks = ceil_div(tiles, kSpChunk);
-    const size_t arr = ((tiles + 2) * 4 + 255) / 256 * 256;
+    const size_t arr = ((tiles + 2) * 8 + 255) / 256 * 256;
     char* p = static_cast<char*>(ws);
     uint32_t* coords = reinterpret_cast<uint32_t*>(p);
     uint32_t* tile_head = reinterpret_cast<uint32_t*>(p + arr);
-    float* tile_tail = reinterpret_cast<float*>(p + 2 * arr);
+    T* tile_tail = reinterpret_cast<T*>(p + 2 * arr);
     unsigned* chunk_flag = reinterpret_cast<unsigned*>(p + 3 * arr);
-    float* chunk_val = reinterpret_cast<float*>(chunk_flag + chunks);
+    T* chunk_val = reinterpret_cast<T*>(p + 3 * arr + ((chunks + 1) * 4 + 15) / 16 * 16);
     k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
-    k_spmv_merge<<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail);
+    k_spmv_merge<T><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail);
     if (tiles > 1) {
-        k_spmv_chunk_agg<<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val);
-        k_spmv_carry<<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val, y);
+        k_spmv_chunk_agg<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val);
+        k_spmv_carry<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val, y);
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,
+                        uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s) {
+    return launch_spmv_t<float>(offsets, indices, w, x, y, n, m, ws, ws_bytes, s);
+}
+
+cudaError_t launch_spmv_f64(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x,
+                            double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s) {
+    return launch_spmv_t<double>(offsets, indices, w, x, y, n, m, ws, ws_bytes, s);
 }
 
 }  // namespace boba

@@ -119,16 +119,20 @@ def coo_to_csr(I2: torch.Tensor, J2: torch.Tensor, n: int, weights: torch.Tensor
 def spmv(offsets: torch.Tensor, indices: torch.Tensor, x: torch.Tensor,
          weights: torch.Tensor | None = None, out: torch.Tensor | None = None,
          ws: torch.Tensor | None = None) -> torch.Tensor:
-    """Phase 5 (reference kernels.py:30-52), fp32."""
+    """Phase 5 (reference kernels.py:30-52).  Computes in x's precision:
+    float32 (the benchmarked path) or float64 (the reference's)."""
     n = offsets.numel() - 1
     m = indices.numel()
-    x = x.to(torch.float32).contiguous()
+    f64 = x.dtype == torch.float64
+    dt = torch.float64 if f64 else torch.float32
+    x = x.to(dt).contiguous()
     if weights is not None:
-        weights = weights.to(torch.float32).contiguous()
-    y = out if out is not None else torch.empty(max(n, 1), dtype=torch.float32, device=offsets.device)[:n]
+        weights = weights.to(dt).contiguous()
+    y = out if out is not None else torch.empty(max(n, 1), dtype=dt, device=offsets.device)[:n]
     if ws is None:
         ws = _ws(N.lib.boba_spmv_workspace_size(n, m), offsets.device)
-    N.check(N.lib.boba_spmv(_p(offsets), _p(indices), _p(weights), _p(x), _p(y), n, m, _p(ws), ws.numel(), _s()))
+    fn = N.lib.boba_spmv_f64 if f64 else N.lib.boba_spmv
+    N.check(fn(_p(offsets), _p(indices), _p(weights), _p(x), _p(y), n, m, _p(ws), ws.numel(), _s()))
     return y
 
 

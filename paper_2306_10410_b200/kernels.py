@@ -1,11 +1,12 @@
 """CSR SpMV on the GPU with the reference's API (pkg/src/boba/kernels.py).
 
 ``spmv_pull`` mirrors kernels.py:30-52: y[v] = sum over row v of
-w * x[indices], empty rows 0, ValueError on a length mismatch.  The
-arithmetic is fp32 on the device (merge-path kernel, deterministic); the
-result is returned as float64 like the reference's.  Parity with the
-reference's float64 sums is a tolerance check (1e-5 relative for
-non-negative x; exact when every partial sum is an integer below 2^24).
+w * x[indices], empty rows 0, ValueError on a length mismatch.  It runs the
+merge-path kernel in float64 -- the reference's precision -- so it agrees
+with the reference to fp64 rounding (the reference's np.add.reduceat has its
+own summation order, so not bit for bit unless the sums are exact).  The
+benchmarked path is the fp32 instantiation of the same kernel
+(``device.spmv`` with float32 x; 1e-5 relative, SURVEY.md §7 hard part 6).
 """
 
 from __future__ import annotations

@@ -46,10 +46,10 @@ def run_case(bb, c):
     if c["w"] is not None:
         assert np.array_equal(csr.weights, c["w2"]) and np.array_equal(raw.weights, c["w2_raw"])
     assert np.array_equal(bb.degrees(g), c["deg"])
-    y = bb.spmv_pull(csr, c["x"])
-    np.testing.assert_allclose(y, c["y"], rtol=SPMV_RTOL, atol=1e-6)
+    y = bb.spmv_pull(csr, c["x"])           # float64 path: the reference's precision
+    np.testing.assert_allclose(y, c["y"], rtol=1e-12, atol=1e-12)
     y0 = bb.spmv_pull(raw, c["x"])
-    np.testing.assert_allclose(y0, c["y_raw"], rtol=SPMV_RTOL, atol=1e-6)
+    np.testing.assert_allclose(y0, c["y_raw"], rtol=1e-12, atol=1e-12)
 
 
 def test_known_answers(bb, kat):
@@ -180,9 +180,12 @@ def test_rmat_pipeline_bit_exact(dev, scale, ef):
     I, J = dev.gather(lab, I), dev.gather(lab, J)
     pipe, off, idx = pipeline_vs_oracle(dev, I, J, n)
     x = np.random.default_rng(5).random(n)
-    y = dev.spmv(pipe.offsets[: n + 1], pipe.indices[: I.numel()], torch.from_numpy(x).cuda())
+    xs = torch.from_numpy(x).cuda()
     want = oracle.spmv_pull(off, idx, x)
+    y = dev.spmv(pipe.offsets[: n + 1], pipe.indices[: I.numel()], xs.float())   # fp32 (bench path)
     np.testing.assert_allclose(y.cpu().numpy(), want, rtol=SPMV_RTOL, atol=1e-5)
+    y64 = dev.spmv(pipe.offsets[: n + 1], pipe.indices[: I.numel()], xs)         # fp64 (drop-in path)
+    np.testing.assert_allclose(y64.cpu().numpy(), want, rtol=1e-12, atol=1e-12)
 
 
 def test_grid_pipeline_bit_exact(dev):
