@@ -26,10 +26,10 @@ struct RadixCfg {
     static constexpr int NW = NT / 32;
     static constexpr int TILE = NT * IPT;
     static constexpr int BPT = B >= NT ? B / NT : 1;              // digits per thread in the scans
-    static constexpr int HIST_BYTES = NW * B * 2;                  // 16-bit warp counters
-    static constexpr int STAGE_BYTES = TILE * 8;                   // keys + payloads
-    static constexpr int REGION = HIST_BYTES > STAGE_BYTES ? HIST_BYTES : STAGE_BYTES;
-    static constexpr size_t SMEM = (size_t)REGION + 2 * B * 4;     // + s_off, s_glob
+    static constexpr int HIST_BYTES = (NW * B * 2 + 15) / 16 * 16;  // 16-bit warp counters
+    static constexpr int STAGE_BYTES = TILE * 8;                    // staged keys + payloads
+    static constexpr int RAW_BYTES = TILE * 4;                      // payloads prefetched by cp.async
+    static constexpr size_t SMEM = (size_t)HIST_BYTES + STAGE_BYTES + RAW_BYTES + 2 * B * 4;  // + s_off, s_glob
     static_assert(TILE < 65536, "16-bit counters and packed ranks");
     static_assert(B % NT == 0 || NT % B == 0, "digit ownership");
 };
@@ -116,11 +116,12 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     using C = RadixCfg<RB, NT, IPT>;
     constexpr int B = C::B, NW = C::NW, TILE = C::TILE, BPT = C::BPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint16_t* s_hist = reinterpret_cast<uint16_t*>(smem_raw);            // NW x B warp counters
-    uint32_t* s_key = reinterpret_cast<uint32_t*>(smem_raw);             // TILE (aliases s_hist later)
-    uint32_t* s_val = s_key + TILE;                                      // TILE
-    uint32_t* s_off = reinterpret_cast<uint32_t*>(smem_raw + C::REGION); // B: tile-local digit offsets
-    uint32_t* s_glob = s_off + B;                                        // B: global position - s_off
+    uint16_t* s_hist = reinterpret_cast<uint16_t*>(smem_raw);                  // NW x B warp counters
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(smem_raw + C::HIST_BYTES);   // TILE staged keys
+    uint32_t* s_val = s_key + TILE;                                            // TILE staged payloads
+    uint32_t* s_raw = s_val + TILE;                                            // TILE payloads, input order
+    uint32_t* s_off = s_raw + TILE;                                            // B: tile-local digit offsets
+    uint32_t* s_glob = s_off + B;                                              // B: global position - s_off
     __shared__ uint32_t s_scan[NW + 1];
 
     const int nb = 1 << bits;
@@ -132,6 +133,29 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     const bool full = tile_base + TILE <= m;
 
     for (int i = threadIdx.x; i < NW * B / 2; i += NT) reinterpret_cast<uint32_t*>(s_hist)[i] = 0;
+    // Prefetch this warp's payload run (IPT*32 words) into shared memory with
+    // cp.async; it lands while the warp ranks its keys.
+    uint32_t* wraw = s_raw + warp * 32 * IPT;
+    if (vals_in) {
+        if (full && ((reinterpret_cast<uintptr_t>(vals_in + wslot) & 15) == 0)) {
+#pragma unroll
+            for (int c = lane; c < IPT * 8; c += 32) {
+                const unsigned saddr = (unsigned)__cvta_generic_to_shared(wraw + 4 * c);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(vals_in + wslot + 4 * c)
+                             : "memory");
+            }
+        } else {
+            for (int c = lane; c < IPT * 32; c += 32) {
+                const uint64_t idx = wslot + (uint64_t)c;
+                if (idx < m) {
+                    const unsigned saddr = (unsigned)__cvta_generic_to_shared(wraw + c);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(saddr), "l"(vals_in + idx)
+                                 : "memory");
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
     uint32_t key[IPT], rank[IPT];
     if (full) {
 #pragma unroll
@@ -151,11 +175,21 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
         const bool ok = full || wslot + (uint64_t)i * 32 + lane < m;
         const uint32_t d = (key[i] >> shift) & mask;
         unsigned peers = full ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, ok);
+        // peers &= lanes whose digit bit b equals mine, for every bit b:
+        // one predicate test, one ballot and one predicated AND per bit.
 #pragma unroll
         for (int b = 0; b < RB; b++) {  // bits >= `bits` are zero in every lane: no effect
-            const unsigned bb = __ballot_sync(0xFFFFFFFFu, (d >> b) & 1u);
-            const unsigned t = 0u - ((d >> b) & 1u);
-            peers &= ~(bb ^ t);
+            asm("{\n\t"
+                ".reg .pred p;\n\t"
+                ".reg .b32 bb;\n\t"
+                "and.b32 bb, %1, %2;\n\t"
+                "setp.ne.u32 p, bb, 0;\n\t"
+                "vote.sync.ballot.b32 bb, p, 0xffffffff;\n\t"
+                "@!p not.b32 bb, bb;\n\t"
+                "and.b32 %0, %0, bb;\n\t"
+                "}"
+                : "+r"(peers)
+                : "r"(d), "r"(1u << b));
         }
         const unsigned below = peers & lt;
         uint32_t pre = 0;
@@ -206,13 +240,13 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
             rank[i] += s_off[d] + wh[d];
         }
     }
-    __syncthreads();  // s_hist is dead; the staging buffers alias it
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
         if (rank[i] != 0xFFFFFFFFu) {
-            const uint64_t idx = wslot + (uint64_t)i * 32 + lane;
             s_key[rank[i]] = key[i];
-            s_val[rank[i]] = vals_in ? __ldg(vals_in + idx) : (uint32_t)idx;  // payload read late
+            s_val[rank[i]] = vals_in ? wraw[i * 32 + lane] : (uint32_t)(wslot + (uint64_t)i * 32 + lane);
         }
     }
     __syncthreads();
