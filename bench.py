@@ -206,12 +206,10 @@ def run_ours(args):
     from paper_2306_10410_b200 import _native as N
     from paper_2306_10410_b200 import device as D
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
+    world = 1  # N > 1 runs the sharded pipeline (run_sharded)
+    rank = 0
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     cfg = args.config
     kind, p, desc = CONFIGS[cfg]
@@ -419,6 +417,131 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_sharded(args):
+    """N GPUs (or --sharded on 1): the multi-GPU pipeline of
+    paper_2306_10410_b200.sharded over contiguous edge shards.  Weak scaling
+    for R-MAT configs: scale = config scale + log2(N), so every GPU holds the
+    config's edge count (c2: 67M edges per GPU)."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2306_10410_b200 import device as D
+    from paper_2306_10410_b200.sharded import shard_range, sharded_reorder_to_csr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    kind, p, desc = CONFIGS[args.config]
+    if kind != "rmat":
+        raise SystemExit("the sharded path runs the R-MAT configs")
+    scale = p["scale"] + int(round(math.log2(world)))
+    n, m = 1 << scale, p["ef"] << scale
+    e0, e1 = shard_range(m, rank, world)
+    I0, J0 = D.generate_rmat_range(scale, e0, e1 - e0, GEN_SEED, dev)
+    lab = torch.from_numpy(oracle.random_labels(n, LABEL_SEED).astype(np.int32)).to(dev)
+    I, J = D.gather(lab, I0), D.gather(lab, J0)
+    del I0, J0, lab
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        return sharded_reorder_to_csr(I, J, n, m, e0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ts = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            res = step()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+    t = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_total = float(t.item())
+    value = m * args.steps / t_total / 1e9
+    ms_step = 1e3 * t_total / args.steps
+    # sanity on the last step's output (local, cheap)
+    assert int(res.offsets[-1].item()) == res.indices.numel()
+
+    # end to end: pinned host shard -> device, sharded pipeline, local CSR back to host
+    hI = torch.empty(e1 - e0, dtype=torch.int32, pin_memory=True)
+    hJ = torch.empty(e1 - e0, dtype=torch.int32, pin_memory=True)
+    hI.copy_(I)
+    hJ.copy_(J)
+    h_off = torch.empty(res.offsets.numel() + 4096, dtype=torch.int32, pin_memory=True)
+    h_idx = torch.empty(2 * (e1 - e0) + 4096, dtype=torch.int32, pin_memory=True)
+    te = []
+    for k in range(max(3, min(args.steps, 5))):
+        dist.barrier()
+        t0 = time.perf_counter()
+        I.copy_(hI, non_blocking=True)
+        J.copy_(hJ, non_blocking=True)
+        r2 = step()
+        no, ni = r2.offsets.numel(), r2.indices.numel()
+        if no <= h_off.numel():
+            h_off[:no].copy_(r2.offsets, non_blocking=True)
+        if ni <= h_idx.numel():
+            h_idx[:ni].copy_(r2.indices, non_blocking=True)
+        torch.cuda.synchronize()
+        te.append(time.perf_counter() - t0)
+    et = torch.tensor([sum(te) / len(te)], dtype=torch.float64, device=dev)
+    dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    t_e2e = float(et.item())
+    hbm, peak_kind = peaks()
+    per_gpu_alg = sum(alg_bytes(m, n).values()) / world
+    line = {
+        "metric": "BOBA reorder+COO->CSR GEdges/s",
+        "value": round(value, 3),
+        "unit": "GEdges/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": f"R-MAT scale {scale} edge factor {p['ef']} sharded over {world} GPU(s), randomly "
+                               f"relabelled (weak scaling from {desc})", "n": n, "m": m,
+                   "parallelism": f"edge-shard{world}: allreduce-MIN + all-to-all by row range (NCCL)",
+                   "l2": "256 MiB L2 flush between steps"},
+        "roofline": {"bound": "hbm", "kernel": "sharded_step", "achieved": round(per_gpu_alg / (ms_step / 1e3) / 1e9, 1),
+                     "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(per_gpu_alg / (ms_step / 1e3) / 1e9 / hbm, 4), "traffic": None,
+                     "note": "per-GPU share of SURVEY §8d algorithmic bytes over the whole step incl. collectives"},
+        "cpu_baseline": None,
+        "e2e": {"value": round(m / t_e2e / 1e9, 4), "unit": "GEdges/s", "ms_per_step": round(1e3 * t_e2e, 3),
+                "h2d_bytes_per_step": 8 * m, "d2h_bytes_per_step": int(4 * (n + world) + 4 * m),
+                "path": "pinned host shards -> sharded pipeline -> row-partitioned CSR to host"},
+        # first-hit, 2x bias, mark/scan/assign, relabel, degrees, scan, range partition (4),
+        # offset ids, local CSR (3 per radix pass + row starts + suffix-min)
+        "gpu_launches": args.steps * (1 + 2 + 3 + 1 + 1 + 1 + 4 + 1
+                                      + 3 * csr_passes(max(res.row_hi - res.row_lo, 1)) + 2),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def csr_passes(n):
     bits = 0 if n <= 1 else (n - 1).bit_length()
     maxb = 11 if os.environ.get("BOBA_RADIX_CFG", "a").startswith("1") else 8
@@ -441,9 +564,12 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded pipeline even on 1 GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded:
+        run_sharded(args)
     else:
         run_ours(args)
 

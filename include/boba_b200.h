@@ -58,6 +58,16 @@ const char *boba_last_error(void);
 int boba_first_occurrence(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n,
                           uint32_t *first, int relaxed, void *stream);
 
+/* Multi-GPU shard of phase 1: this rank holds edges
+ * [e0, e0 + m_local) of a global list of m_global edges; local I[i] is global
+ * position e0 + i and local J[i] is m_global + e0 + i.  Merging the per-rank
+ * arrays with an elementwise min (NCCL allreduce-MIN after boba_bias_u32)
+ * gives exactly boba_first_occurrence of the whole list -- the reference's
+ * chunk-local-min merge, _parallel.py:139-162. */
+int boba_first_occurrence_shard(const uint32_t *I, const uint32_t *J, uint64_t m_local,
+                                uint64_t m_global, uint64_t e0, uint32_t n, uint32_t *first,
+                                int relaxed, void *stream);
+
 /* --- Phase 2: rank compaction -> permutation --------------------------
  * order[k] = the vertex with the k-th smallest first[] value, then the
  * vertices with first == UNSET in ascending id; label[order[k]] = k.
@@ -150,12 +160,35 @@ int boba_ctx_reorder_to_csr_host(boba_ctx *ctx, const uint32_t *I_host, const ui
 int boba_narrow_ids(const int64_t *in, uint64_t count, uint64_t bound, uint32_t *out,
                     int64_t *bad_index, void *stream);
 int boba_widen_ids(const uint32_t *in, uint64_t count, int64_t *out, void *stream);
+/* offsets[0..n] = exclusive prefix sum of counts[0..n) (offsets[n] = total):
+ * np.cumsum of graph.py:270-272 on the device. */
+size_t boba_exclusive_scan_workspace_size(uint64_t count);
+int boba_exclusive_scan_u32(const uint32_t *counts, uint32_t n, uint32_t *offsets, void *workspace,
+                            size_t workspace_bytes, void *stream);
+/* out[i] = in[i] ^ 0x80000000: an order-preserving map from uint32 to int32
+ * (UNSET stays the maximum), so first[] can be merged with a signed MIN
+ * collective. Its own inverse. */
+int boba_bias_u32(const uint32_t *in, uint64_t count, uint32_t *out, void *stream);
+/* out[i] = in[i] + delta (mod 2^32): shift global row ids to a local range. */
+int boba_offset_ids(const uint32_t *in, uint64_t count, uint32_t delta, uint32_t *out, void *stream);
+/* Stable partition of (key, val) pairs by key range: part p holds the keys in
+ * [bounds[p], bounds[p+1]) (bounds: parts+1 ascending device uint32, only
+ * bounds[1..parts-1] are read), in input order; counts_out[p] (device) = pairs
+ * in part p.  The send side of the multi-GPU all-to-all by row range. */
+size_t boba_range_partition_workspace_size(uint64_t m, int parts);
+int boba_range_partition(const uint32_t *keys, const uint32_t *vals, uint64_t m,
+                         const uint32_t *bounds, int parts, uint32_t *keys_out, uint32_t *vals_out,
+                         uint32_t *counts_out, void *workspace, size_t workspace_bytes,
+                         void *stream);
 /* out[i] = src[idx[i]] (permutation application on vertex arrays). */
 int boba_gather_u32(const uint32_t *src, const uint32_t *idx, uint64_t count, uint32_t *out,
                     void *stream);
 /* Graph500 R-MAT (a,b,c,d = .57,.19,.19,.05), m = edge_factor << scale
  * i.i.d. edges in generation order; identical to oracle_rmat_edges. */
 int boba_generate_rmat(int scale, uint64_t m, uint64_t seed, uint32_t *I, uint32_t *J, void *stream);
+/* Edges [e0, e0 + count) of the same stream (for per-rank shards). */
+int boba_generate_rmat_range(int scale, uint64_t e0, uint64_t count, uint64_t seed, uint32_t *I,
+                             uint32_t *J, void *stream);
 /* 4-neighbour grid, reference generators.py:100-111 generate_grid. */
 int boba_generate_grid(uint32_t rows, uint32_t cols, uint32_t *I, uint32_t *J, void *stream);
 

@@ -37,6 +37,7 @@ SIGNATURES = {
     "boba_abi_version": ([], _I),
     "boba_last_error": ([], ctypes.c_char_p),
     "boba_first_occurrence": ([_P, _P, _U64, _U32, _P, _I, _P], _I),
+    "boba_first_occurrence_shard": ([_P, _P, _U64, _U64, _U64, _U32, _P, _I, _P], _I),
     "boba_compact_workspace_size": ([_U64, _U32], _SZ),
     "boba_compact": ([_P, _U64, _U32, _P, _P, _P, _P, _SZ, _P], _I),
     "boba_order_workspace_size": ([_U64, _U32], _SZ),
@@ -56,8 +57,15 @@ SIGNATURES = {
     "boba_ctx_reorder_to_csr_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P], _I),
     "boba_narrow_ids": ([_P, _U64, _U64, _P, ctypes.POINTER(ctypes.c_int64), _P], _I),
     "boba_widen_ids": ([_P, _U64, _P, _P], _I),
+    "boba_exclusive_scan_workspace_size": ([_U64], _SZ),
+    "boba_exclusive_scan_u32": ([_P, _U32, _P, _P, _SZ, _P], _I),
+    "boba_bias_u32": ([_P, _U64, _P, _P], _I),
+    "boba_offset_ids": ([_P, _U64, _U32, _P, _P], _I),
+    "boba_range_partition_workspace_size": ([_U64, _I], _SZ),
+    "boba_range_partition": ([_P, _P, _U64, _P, _I, _P, _P, _P, _P, _SZ, _P], _I),
     "boba_gather_u32": ([_P, _P, _U64, _P, _P], _I),
     "boba_generate_rmat": ([_I, _U64, _U64, _P, _P, _P], _I),
+    "boba_generate_rmat_range": ([_I, _U64, _U64, _U64, _P, _P, _P], _I),
     "boba_generate_grid": ([_U32, _U32, _P, _P, _P], _I),
 }
 

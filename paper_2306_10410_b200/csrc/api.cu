@@ -84,6 +84,18 @@ int boba_first_occurrence(const uint32_t* I, const uint32_t* J, uint64_t m, uint
                        "boba_first_occurrence");
 }
 
+int boba_first_occurrence_shard(const uint32_t* I, const uint32_t* J, uint64_t m_local, uint64_t m_global,
+                                uint64_t e0, uint32_t n, uint32_t* first, int relaxed, void* stream) {
+    if (int rc = check_sizes(m_global, n, "boba_first_occurrence_shard")) return rc;
+    REQUIRE(e0 + m_local <= m_global, "boba_first_occurrence_shard: shard [e0, e0+m_local) outside [0, m_global)");
+    REQUIRE(first || n == 0, "boba_first_occurrence_shard: first is NULL");
+    REQUIRE((I && J) || m_local == 0, "boba_first_occurrence_shard: I/J is NULL");
+    if (n == 0) return BOBA_OK;
+    return cuda_status(boba::launch_first_hit_shard(I, J, m_local, m_global, e0, n, first, relaxed != 0, num_sms(),
+                                                    S(stream)),
+                       "boba_first_occurrence_shard");
+}
+
 size_t boba_compact_workspace_size(uint64_t m, uint32_t n) { return boba::compact_workspace_bytes(m, n); }
 
 int boba_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order, uint32_t* label,
@@ -295,6 +307,47 @@ int boba_widen_ids(const uint32_t* in, uint64_t count, int64_t* out, void* strea
     return cuda_status(boba::launch_widen(in, count, out, num_sms(), S(stream)), "boba_widen_ids");
 }
 
+size_t boba_exclusive_scan_workspace_size(uint64_t count) {
+    return (boba::ceil_div(count + 1, 2048) + 2) * 8 + 256;
+}
+
+int boba_exclusive_scan_u32(const uint32_t* counts, uint32_t n, uint32_t* offsets, void* ws, size_t ws_bytes,
+                            void* stream) {
+    REQUIRE(offsets && ws && (counts || n == 0), "boba_exclusive_scan_u32: NULL argument");
+    REQUIRE(n < 0xFFFFFFFFu, "boba_exclusive_scan_u32: n too large");
+    REQUIRE(ws_bytes >= boba_exclusive_scan_workspace_size(n), "boba_exclusive_scan_u32: workspace too small");
+    unsigned long long* st = static_cast<unsigned long long*>(ws);
+    unsigned* counter = reinterpret_cast<unsigned*>(st + boba::ceil_div((uint64_t)n + 1, 2048) + 1);
+    return cuda_status(boba::launch_row_offsets(counts, n, offsets, st, counter, S(stream)),
+                       "boba_exclusive_scan_u32");
+}
+
+int boba_bias_u32(const uint32_t* in, uint64_t count, uint32_t* out, void* stream) {
+    REQUIRE((in && out) || count == 0, "boba_bias_u32: NULL argument");
+    return cuda_status(boba::launch_bias(in, count, out, num_sms(), S(stream)), "boba_bias_u32");
+}
+
+int boba_offset_ids(const uint32_t* in, uint64_t count, uint32_t delta, uint32_t* out, void* stream) {
+    REQUIRE((in && out) || count == 0, "boba_offset_ids: NULL argument");
+    return cuda_status(boba::launch_offset_ids(in, count, delta, out, num_sms(), S(stream)), "boba_offset_ids");
+}
+
+size_t boba_range_partition_workspace_size(uint64_t m, int parts) {
+    return boba::range_partition_workspace_bytes(m, parts);
+}
+
+int boba_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds, int parts,
+                         uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out, void* ws, size_t ws_bytes,
+                         void* stream) {
+    REQUIRE(parts >= 1 && parts <= 256, "boba_range_partition: parts must be in [1, 256]");
+    REQUIRE(bounds && counts_out && ws, "boba_range_partition: NULL argument");
+    REQUIRE((keys && vals && keys_out && vals_out) || m == 0, "boba_range_partition: NULL edge arrays");
+    REQUIRE(m < 0xFFFFFFFFull, "boba_range_partition: m too large");
+    return cuda_status(boba::launch_range_partition(keys, vals, m, bounds, parts, keys_out, vals_out, counts_out, ws,
+                                                    ws_bytes, num_sms(), S(stream)),
+                       "boba_range_partition");
+}
+
 int boba_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, void* stream) {
     REQUIRE((src && idx && out) || count == 0, "boba_gather_u32: NULL argument");
     return cuda_status(boba::launch_gather_u32(src, idx, count, out, num_sms(), S(stream)), "boba_gather_u32");
@@ -303,7 +356,15 @@ int boba_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, ui
 int boba_generate_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32_t* J, void* stream) {
     REQUIRE(scale >= 0 && scale <= 32, "boba_generate_rmat: scale out of range");
     REQUIRE((I && J) || m == 0, "boba_generate_rmat: NULL argument");
-    return cuda_status(boba::launch_rmat(scale, m, seed, I, J, num_sms(), S(stream)), "boba_generate_rmat");
+    return cuda_status(boba::launch_rmat(scale, 0, m, seed, I, J, num_sms(), S(stream)), "boba_generate_rmat");
+}
+
+int boba_generate_rmat_range(int scale, uint64_t e0, uint64_t count, uint64_t seed, uint32_t* I, uint32_t* J,
+                             void* stream) {
+    REQUIRE(scale >= 0 && scale <= 32, "boba_generate_rmat_range: scale out of range");
+    REQUIRE((I && J) || count == 0, "boba_generate_rmat_range: NULL argument");
+    return cuda_status(boba::launch_rmat(scale, e0, count, seed, I, J, num_sms(), S(stream)),
+                       "boba_generate_rmat_range");
 }
 
 int boba_generate_grid(uint32_t rows, uint32_t cols, uint32_t* I, uint32_t* J, void* stream) {

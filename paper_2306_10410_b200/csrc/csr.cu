@@ -257,14 +257,14 @@ CsrWs carve(void* base, uint64_t m, uint32_t n) {
     return w;
 }
 
-template <int RB, int NT, int IPT, int MINB>
-cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits, uint32_t* H,
-                       unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                       int num_sms, cudaStream_t s) {
+template <int RB, int NT, int IPT, int MINB, typename Op = DigitShift>
+cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, Op op, int bits, uint32_t* H,
+                          unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
+                          int num_sms, cudaStream_t s) {
     using C = RadixCfg<RB, NT, IPT>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_radix_downsweep<RB, NT, IPT, MINB>,
+        cudaError_t e = cudaFuncSetAttribute(k_radix_downsweep<RB, NT, IPT, MINB, Op>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         if (e != cudaSuccess) return e;
         attr_set = true;
@@ -272,14 +272,22 @@ cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int
     const uint64_t tiles = ceil_div(m, C::TILE);
     const uint64_t hcount = tiles << bits;
     const uint64_t up_grid = tiles < (uint64_t)num_sms * 8 ? tiles : (uint64_t)num_sms * 8;
-    k_radix_upsweep<RB, NT, IPT><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, shift, bits, tiles, H);
+    k_radix_upsweep<RB, NT, IPT, Op><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, op, bits, tiles, H);
     cudaError_t e = cudaMemsetAsync(scan_status, 0, (ceil_div(hcount, kScanTile) + 1) * 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 4, s);
     if (e != cudaSuccess) return e;
     k_scan_u32<<<(unsigned)ceil_div(hcount, kScanTile), kScanTileNT, 0, s>>>(H, hcount, 0u, scan_status, counter);
-    k_radix_downsweep<RB, NT, IPT, MINB><<<(unsigned)tiles, NT, C::SMEM, s>>>(kin, vin, m, shift, bits, tiles, H,
-                                                                            kout, vout);
+    k_radix_downsweep<RB, NT, IPT, MINB, Op><<<(unsigned)tiles, NT, C::SMEM, s>>>(kin, vin, m, op, bits, tiles, H,
+                                                                                kout, vout);
     return cudaGetLastError();
+}
+
+template <int RB, int NT, int IPT, int MINB>
+cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits, uint32_t* H,
+                       unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
+                       int num_sms, cudaStream_t s) {
+    return radix_pass_op<RB, NT, IPT, MINB, DigitShift>(kin, vin, m, DigitShift{shift, (1u << bits) - 1u}, bits, H,
+                                                        scan_status, counter, kout, vout, num_sms, s);
 }
 
 cudaError_t dispatch_pass(Variant v, const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits,
@@ -297,6 +305,50 @@ cudaError_t dispatch_pass(Variant v, const uint32_t* kin, const uint32_t* vin, u
 }  // namespace
 
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool /*weighted*/) { return carve(nullptr, m, n).total; }
+
+// ------------------------------------------------- row-range partition ---
+// Stable partition of (key, payload) pairs by which of `parts` key ranges
+// [bounds[p], bounds[p+1]) the key falls in -- the send side of the
+// multi-GPU all-to-all by destination row range.  One radix pass whose digit
+// is the range index; counts_out[p] = pairs in part p.
+__global__ void k_part_counts(const uint32_t* __restrict__ H, uint64_t tiles, int parts, uint64_t m,
+                              uint32_t* counts) {
+    const int p = threadIdx.x;
+    if (p >= parts) return;
+    const uint32_t lo = H[(uint64_t)p * tiles];
+    const uint32_t hi = p + 1 < parts ? H[(uint64_t)(p + 1) * tiles] : (uint32_t)m;
+    counts[p] = hi - lo;
+}
+
+namespace {
+int part_bits(int parts) { return parts <= 1 ? 1 : 32 - __builtin_clz((unsigned)parts - 1); }
+}
+
+size_t range_partition_workspace_bytes(uint64_t m, int parts) {
+    const uint64_t tiles = ceil_div(m ? m : 1, RadixCfg<8, 256, 16>::TILE);
+    const uint64_t hcount = tiles << part_bits(parts);
+    return ((hcount * 4 + 255) / 256 * 256) + (ceil_div(hcount, kScanTile) + 1) * 8 + 256;
+}
+
+cudaError_t launch_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds,
+                                   int parts, uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out, void* ws,
+                                   size_t ws_bytes, int num_sms, cudaStream_t s) {
+    if (parts < 1 || parts > 256) return cudaErrorInvalidValue;
+    if (ws_bytes < range_partition_workspace_bytes(m, parts)) return cudaErrorInvalidValue;
+    if (m == 0) return cudaMemsetAsync(counts_out, 0, (size_t)parts * 4, s);
+    const int bits = part_bits(parts);
+    const uint64_t tiles = ceil_div(m, RadixCfg<8, 256, 16>::TILE);
+    const uint64_t hcount = tiles << bits;
+    char* p = static_cast<char*>(ws);
+    uint32_t* H = reinterpret_cast<uint32_t*>(p);
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(p + (hcount * 4 + 255) / 256 * 256);
+    unsigned* counter = reinterpret_cast<unsigned*>(st + ceil_div(hcount, kScanTile) + 1);
+    cudaError_t e = radix_pass_op<8, 256, 16, 4, DigitRange>(keys, vals, m, DigitRange{bounds, parts}, bits, H, st,
+                                                             counter, keys_out, vals_out, num_sms, s);
+    if (e != cudaSuccess) return e;
+    k_part_counts<<<1, 256, 0, s>>>(H, tiles, parts, m, counts_out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_row_offsets(const uint32_t* counts, uint32_t n, uint32_t* offsets, unsigned long long* status,
                                unsigned* counter, cudaStream_t s) {

@@ -51,7 +51,7 @@ __device__ __forceinline__ void hit(uint32_t* first, uint32_t* set, uint32_t v, 
 template <bool RELAXED>
 __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(const uint32_t* __restrict__ I,
                                                         const uint32_t* __restrict__ J, uint64_t m,
-                                                        uint32_t* first) {
+                                                        uint32_t base_i, uint32_t base_j, uint32_t* first) {
     extern __shared__ uint32_t set[];
     for (int i = threadIdx.x; i < (1 << kFhSlotsLog2); i += kFhNT) set[i] = kEmpty;
     const uint64_t quads = m >> 2;          // full 16-byte quads per array
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(const uint32_t* __restri
         __syncthreads();  // every warp has left the previous iteration
         const uint64_t q0 = it * kFhNT * kFhQuads;
         // lowest position of this iteration (quads of J start at position m)
-        const uint32_t iter_lo = (uint32_t)(q0 < quads ? 4 * q0 : m + 4 * (q0 - quads));
+        const uint32_t iter_lo = (uint32_t)(q0 < quads ? base_i + 4 * q0 : base_j + 4 * (q0 - quads));
         uint4 q[kFhQuads];
         uint32_t pos[kFhQuads];
         bool ok[kFhQuads];
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(const uint32_t* __restri
                 const bool inJ = w >= quads;
                 const uint64_t qi = inJ ? w - quads : w;
                 q[k] = __ldg(reinterpret_cast<const uint4*>(inJ ? J : I) + qi);
-                pos[k] = (uint32_t)(4 * qi + (inJ ? m : 0));
+                pos[k] = (uint32_t)(4 * qi) + (inJ ? base_j : base_i);
             }
         }
 #pragma unroll
@@ -90,14 +90,14 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(const uint32_t* __restri
 // Scalar path: unaligned inputs and the (m mod 4) tails.
 template <bool RELAXED>
 __global__ void k_first_hit_scalar(const uint32_t* __restrict__ I, const uint32_t* __restrict__ J, uint64_t e0,
-                                   uint64_t m, uint32_t* first) {
+                                   uint64_t m, uint32_t base_i, uint32_t base_j, uint32_t* first) {
     const uint64_t cnt = m - e0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * cnt; t += stride) {
         const bool inJ = t >= cnt;
         const uint64_t e = e0 + (inJ ? t - cnt : t);
         const uint32_t v = inJ ? J[e] : I[e];
-        const uint32_t pos = (uint32_t)(e + (inJ ? m : 0));
+        const uint32_t pos = (uint32_t)e + (inJ ? base_j : base_i);
         if (RELAXED) {
             if (pos < *((volatile uint32_t*)(first + v))) *((volatile uint32_t*)(first + v)) = pos;
         } else {
@@ -108,6 +108,14 @@ __global__ void k_first_hit_scalar(const uint32_t* __restrict__ I, const uint32_
 
 cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
                              bool relaxed, int num_sms, cudaStream_t s) {
+    return launch_first_hit_shard(I, J, m, m, 0, n, first, relaxed, num_sms, s);
+}
+
+// A contiguous shard [e0, e0 + m) of a global edge list with m_global edges:
+// local I[i] sits at global position e0 + i, local J[i] at m_global + e0 + i.
+cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_t m, uint64_t m_global, uint64_t e0,
+                                   uint32_t n, uint32_t* first, bool relaxed, int num_sms, cudaStream_t s) {
+    const uint32_t base_i = (uint32_t)e0, base_j = (uint32_t)(m_global + e0);
     cudaError_t err = cudaMemsetAsync(first, 0xFF, (size_t)n * sizeof(uint32_t), s);
     if (err != cudaSuccess || m == 0) return err;
     const bool vec = ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(J)) & 15) == 0;
@@ -123,18 +131,18 @@ cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, u
         const uint64_t iters = ceil_div(2 * (m >> 2), (uint64_t)kFhNT * kFhQuads);
         const int grid = (int)(iters < (uint64_t)num_sms ? iters : (uint64_t)num_sms);
         if (relaxed)
-            k_first_hit<true><<<grid, kFhNT, smem, s>>>(I, J, m, first);
+            k_first_hit<true><<<grid, kFhNT, smem, s>>>(I, J, m, base_i, base_j, first);
         else
-            k_first_hit<false><<<grid, kFhNT, smem, s>>>(I, J, m, first);
+            k_first_hit<false><<<grid, kFhNT, smem, s>>>(I, J, m, base_i, base_j, first);
         done = m & ~3ull;
     }
     if (done < m) {
         uint64_t work = 2 * (m - done), blocks = ceil_div(work, 256), cap = (uint64_t)num_sms * 8;
         int grid = (int)(blocks < cap ? blocks : cap);
         if (relaxed)
-            k_first_hit_scalar<true><<<grid, 256, 0, s>>>(I, J, done, m, first);
+            k_first_hit_scalar<true><<<grid, 256, 0, s>>>(I, J, done, m, base_i, base_j, first);
         else
-            k_first_hit_scalar<false><<<grid, 256, 0, s>>>(I, J, done, m, first);
+            k_first_hit_scalar<false><<<grid, 256, 0, s>>>(I, J, done, m, base_i, base_j, first);
     }
     return cudaGetLastError();
 }

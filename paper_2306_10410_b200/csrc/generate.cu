@@ -21,9 +21,10 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 }
 constexpr uint32_t kTA = 2448131358u, kTB = 3264175144u, kTC = 4080218931u;
 
-__global__ void k_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32_t* J) {
+__global__ void k_rmat(int scale, uint64_t e0, uint64_t count, uint64_t seed, uint32_t* I, uint32_t* J) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const uint64_t e = e0 + i;
         uint64_t key = splitmix64(seed ^ splitmix64(e));
         uint32_t u = 0, v = 0;
         for (int lvl = 0; lvl < scale; lvl += 2) {
@@ -38,8 +39,8 @@ __global__ void k_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32
                 v = (v << 1) | bv;
             }
         }
-        I[e] = u;
-        J[e] = v;
+        I[i] = u;
+        J[i] = v;
     }
 }
 
@@ -91,16 +92,28 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* _
         out[i] = __ldg(src + __ldg(idx + i));
 }
 
+__global__ void k_bias(const uint32_t* __restrict__ in, uint64_t count, uint32_t* out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
+        out[i] = __ldg(in + i) ^ 0x80000000u;
+}
+
+__global__ void k_offset_ids(const uint32_t* __restrict__ in, uint64_t count, uint32_t delta, uint32_t* out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
+        out[i] = __ldg(in + i) + delta;
+}
+
 static int grid_for(uint64_t work, int num_sms) {
     uint64_t blocks = ceil_div(work, 256), cap = (uint64_t)num_sms * 16;
     blocks = blocks < cap ? blocks : cap;
     return (int)(blocks ? blocks : 1);
 }
 
-cudaError_t launch_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32_t* J, int num_sms,
-                        cudaStream_t s) {
-    if (m == 0) return cudaSuccess;
-    k_rmat<<<grid_for(m, num_sms), 256, 0, s>>>(scale, m, seed, I, J);
+cudaError_t launch_rmat(int scale, uint64_t e0, uint64_t count, uint64_t seed, uint32_t* I, uint32_t* J,
+                        int num_sms, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    k_rmat<<<grid_for(count, num_sms), 256, 0, s>>>(scale, e0, count, seed, I, J);
     return cudaGetLastError();
 }
 
@@ -122,6 +135,19 @@ cudaError_t launch_narrow(const int64_t* in, uint64_t count, uint64_t bound, uin
 cudaError_t launch_widen(const uint32_t* in, uint64_t count, int64_t* out, int num_sms, cudaStream_t s) {
     if (count == 0) return cudaSuccess;
     k_widen<<<grid_for(count, num_sms), 256, 0, s>>>(in, count, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bias(const uint32_t* in, uint64_t count, uint32_t* out, int num_sms, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    k_bias<<<grid_for(count, num_sms), 256, 0, s>>>(in, count, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_offset_ids(const uint32_t* in, uint64_t count, uint32_t delta, uint32_t* out, int num_sms,
+                              cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    k_offset_ids<<<grid_for(count, num_sms), 256, 0, s>>>(in, count, delta, out);
     return cudaGetLastError();
 }
 

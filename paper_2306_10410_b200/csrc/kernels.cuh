@@ -10,6 +10,9 @@ namespace boba {
 cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
                              bool relaxed, int num_sms, cudaStream_t s);
 
+cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_t m, uint64_t m_global, uint64_t e0,
+                                   uint32_t n, uint32_t* first, bool relaxed, int num_sms, cudaStream_t s);
+
 size_t compact_workspace_bytes(uint64_t m, uint32_t n);
 // hubs (may be NULL): kHubTableBytes table filled for phase 3 (hubs.cuh)
 cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order, uint32_t* label,
@@ -34,11 +37,19 @@ cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const 
 cudaError_t launch_spmv_f64(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x,
                             double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s);
 
-cudaError_t launch_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32_t* J, int num_sms, cudaStream_t s);
+cudaError_t launch_rmat(int scale, uint64_t e0, uint64_t count, uint64_t seed, uint32_t* I, uint32_t* J,
+                        int num_sms, cudaStream_t s);
 cudaError_t launch_grid(uint32_t rows, uint32_t cols, uint32_t* I, uint32_t* J, int num_sms, cudaStream_t s);
 cudaError_t launch_narrow(const int64_t* in, uint64_t count, uint64_t bound, uint32_t* out,
                           unsigned long long* first_bad, int num_sms, cudaStream_t s);
 cudaError_t launch_widen(const uint32_t* in, uint64_t count, int64_t* out, int num_sms, cudaStream_t s);
+cudaError_t launch_bias(const uint32_t* in, uint64_t count, uint32_t* out, int num_sms, cudaStream_t s);
+cudaError_t launch_offset_ids(const uint32_t* in, uint64_t count, uint32_t delta, uint32_t* out, int num_sms,
+                              cudaStream_t s);
+size_t range_partition_workspace_bytes(uint64_t m, int parts);
+cudaError_t launch_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds,
+                                   int parts, uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out, void* ws,
+                                   size_t ws_bytes, int num_sms, cudaStream_t s);
 cudaError_t launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, int num_sms,
                               cudaStream_t s);
 

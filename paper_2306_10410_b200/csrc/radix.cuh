@@ -20,6 +20,23 @@
 
 namespace boba {
 
+// Digit extractors: the LSD passes use a shift/mask digit; the multi-GPU row
+// partition uses the index of the row range a key falls in (bounds[1..parts)).
+struct DigitShift {
+    int shift;
+    uint32_t mask;
+    __device__ __forceinline__ uint32_t operator()(uint32_t k) const { return (k >> shift) & mask; }
+};
+struct DigitRange {
+    const uint32_t* bounds;  // parts + 1 ascending row boundaries (device)
+    int parts;
+    __device__ __forceinline__ uint32_t operator()(uint32_t k) const {
+        uint32_t o = 0;
+        for (int p = 1; p < parts; p++) o += k >= __ldg(bounds + p);
+        return o;
+    }
+};
+
 template <int RB, int NT, int IPT>
 struct RadixCfg {
     static constexpr int B = 1 << RB;
@@ -35,13 +52,12 @@ struct RadixCfg {
 };
 
 // ------------------------------------------------------------- upsweep ---
-template <int RB, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_radix_upsweep(const uint32_t* __restrict__ keys, uint64_t m, int shift,
+template <int RB, int NT, int IPT, typename Op>
+__global__ void __launch_bounds__(NT) k_radix_upsweep(const uint32_t* __restrict__ keys, uint64_t m, Op op,
                                                       int bits, uint64_t tiles, uint32_t* __restrict__ H) {
     using C = RadixCfg<RB, NT, IPT>;
     __shared__ uint32_t s_h[C::B];
     const int nb = 1 << bits;
-    const uint32_t mask = (uint32_t)nb - 1u;
     for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         for (int d = threadIdx.x; d < nb; d += NT) s_h[d] = 0;
         __syncthreads();
@@ -51,14 +67,14 @@ __global__ void __launch_bounds__(NT) k_radix_upsweep(const uint32_t* __restrict
 #pragma unroll
             for (int i = 0; i < C::TILE / (4 * NT); i++) {
                 const uint4 q = __ldg(k4 + i * NT + threadIdx.x);
-                atomicAdd(s_h + ((q.x >> shift) & mask), 1u);
-                atomicAdd(s_h + ((q.y >> shift) & mask), 1u);
-                atomicAdd(s_h + ((q.z >> shift) & mask), 1u);
-                atomicAdd(s_h + ((q.w >> shift) & mask), 1u);
+                atomicAdd(s_h + op(q.x), 1u);
+                atomicAdd(s_h + op(q.y), 1u);
+                atomicAdd(s_h + op(q.z), 1u);
+                atomicAdd(s_h + op(q.w), 1u);
             }
         } else {
             for (uint64_t i = base + threadIdx.x; i < m && i < base + C::TILE; i += NT)
-                atomicAdd(s_h + ((__ldg(keys + i) >> shift) & mask), 1u);
+                atomicAdd(s_h + op(__ldg(keys + i)), 1u);
         }
         __syncthreads();
         for (int d = threadIdx.x; d < nb; d += NT) H[(uint64_t)d * tiles + t] = s_h[d];
@@ -106,10 +122,10 @@ __global__ void __launch_bounds__(kScanTileNT) k_scan_u32(uint32_t* data, uint64
 }
 
 // ----------------------------------------------------------- downsweep ---
-template <int RB, int NT, int IPT, int MINB>
+template <int RB, int NT, int IPT, int MINB, typename Op>
 __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in, uint64_t m,
-                                                              int shift, int bits, uint64_t tiles,
+                                                              Op op, int bits, uint64_t tiles,
                                                               const uint32_t* __restrict__ H,
                                                               uint32_t* __restrict__ keys_out,
                                                               uint32_t* __restrict__ vals_out) {
@@ -125,7 +141,6 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     __shared__ uint32_t s_scan[NW + 1];
 
     const int nb = 1 << bits;
-    const uint32_t mask = (uint32_t)nb - 1u;
     const uint64_t tile = blockIdx.x;
     const uint64_t tile_base = tile * TILE;
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -173,7 +188,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
         const bool ok = full || wslot + (uint64_t)i * 32 + lane < m;
-        const uint32_t d = (key[i] >> shift) & mask;
+        const uint32_t d = op(key[i]);
         unsigned peers = full ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, ok);
         // peers &= lanes whose digit bit b equals mine, for every bit b:
         // one predicate test, one ballot and one predicated AND per bit.
@@ -236,7 +251,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
         if (rank[i] != 0xFFFFFFFFu) {
-            const uint32_t d = (key[i] >> shift) & mask;
+            const uint32_t d = op(key[i]);
             rank[i] += s_off[d] + wh[d];
         }
     }
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     const int items = rem < (uint64_t)TILE ? (int)rem : TILE;
     for (int j = threadIdx.x; j < items; j += NT) {
         const uint32_t k = s_key[j];
-        const uint32_t g = s_glob[(k >> shift) & mask] + (uint32_t)j;
+        const uint32_t g = s_glob[op(k)] + (uint32_t)j;
         if (keys_out) keys_out[g] = k;
         vals_out[g] = s_val[j];
     }

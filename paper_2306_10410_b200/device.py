@@ -174,6 +174,15 @@ def generate_rmat(scale: int, edge_factor: int, seed: int, device=None):
     return I, J
 
 
+def generate_rmat_range(scale: int, e0: int, count: int, seed: int, device=None):
+    """Edges [e0, e0 + count) of the R-MAT stream of generate_rmat (a shard)."""
+    dev = device or require_cuda()
+    I = torch.empty(count, dtype=ID, device=dev)
+    J = torch.empty(count, dtype=ID, device=dev)
+    N.check(N.lib.boba_generate_rmat_range(scale, e0, count, seed & (2**64 - 1), _p(I), _p(J), _s()))
+    return I, J
+
+
 def generate_grid(rows: int, cols: int, device=None):
     """reference generators.py:100-111 on the device."""
     dev = device or require_cuda()

@@ -1,0 +1,97 @@
+"""GPU side of the multi-GPU path: the device ops the sharded pipeline uses
+(shard first-occurrence with global offsets, order-preserving bias, range
+partition, id offset, exclusive scan) against their numpy twins, P logical
+shards emulated on one GPU, and the full sharded pipeline through a one-rank
+NCCL group."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+from test_sharded_gloo import NumpyOps, t32, u32
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2306_10410_b200.sharded import DeviceOps
+
+    return DeviceOps()
+
+
+def cu(a):
+    return t32(a).cuda()
+
+
+def host(t):
+    return u32(t.cpu())
+
+
+@pytest.mark.parametrize("P", [2, 4, 7])
+def test_shard_first_occurrence_merges_to_global(ops, P):
+    from paper_2306_10410_b200.sharded import shard_range
+
+    I, J = oracle.rmat_edges(14, 8, seed=9)
+    n, m = 1 << 14, I.size
+    r_ref, _ = oracle.first_hit_order_sequential(I, J, n)
+    want = np.where(r_ref == np.iinfo(np.int64).max, 0xFFFFFFFF, r_ref).astype(np.uint32)
+    npo = NumpyOps()
+    merged = None
+    for k in range(P):
+        e0, e1 = shard_range(m, k, P)
+        f = ops.first_occurrence_shard(cu(I[e0:e1]), cu(J[e0:e1]), m, e0, n)
+        assert np.array_equal(host(f), u32(npo.first_occurrence_shard(t32(I[e0:e1]), t32(J[e0:e1]), m, e0, n)))
+        b = host(ops.bias(f)).view(np.int32)
+        merged = b if merged is None else np.minimum(merged, b)   # the allreduce-MIN, signed
+    got = host(ops.bias(cu(merged.view(np.uint32))))
+    assert np.array_equal(got, want)
+
+
+def test_range_partition_and_helpers(ops):
+    rng = np.random.default_rng(4)
+    n, m = 5000, 40001
+    keys = rng.integers(0, n, m)
+    vals = rng.integers(0, 1 << 31, m)
+    bounds = np.array([0, 0, 1200, 1201, 4000, n])        # includes an empty part
+    npo = NumpyOps()
+    ko, vo, c = ops.range_partition(cu(keys), cu(vals), cu(bounds), 5)
+    wk, wv, wc = npo.range_partition(t32(keys), t32(vals), t32(bounds), 5)
+    assert np.array_equal(host(ko), u32(wk)) and np.array_equal(host(vo), u32(wv))
+    assert np.array_equal(host(c), u32(wc))
+    assert np.array_equal(host(ops.offset_ids(cu(keys), -1200)), u32(npo.offset_ids(t32(keys), -1200)))
+    counts = np.bincount(keys, minlength=n)
+    assert np.array_equal(host(ops.exclusive_scan(cu(counts))), u32(npo.exclusive_scan(t32(counts))))
+
+
+def test_sharded_pipeline_one_rank_nccl(ops):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_10410_b200.sharded import sharded_reorder_to_csr
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        I, J = oracle.rmat_edges(16, 8, seed=2)
+        n = 1 << 16
+        lab = oracle.random_labels(n, 7)
+        I, J = lab[I], lab[J]
+        res = sharded_reorder_to_csr(cu(I), cu(J), n, I.size, 0)
+        order, label, I2, J2, off, idx, _ = oracle.pipeline(I, J, n)
+        assert np.array_equal(host(res.order), order) and np.array_equal(host(res.label), label)
+        assert np.array_equal(host(res.I2), I2) and np.array_equal(host(res.J2), J2)
+        assert (res.row_lo, res.row_hi) == (0, n)
+        assert np.array_equal(host(res.offsets), off) and np.array_equal(host(res.indices), idx)
+    finally:
+        dist.destroy_process_group()
