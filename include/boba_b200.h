@@ -63,10 +63,13 @@ int boba_first_occurrence(const uint32_t *I, const uint32_t *J, uint64_t m, uint
  * position e0 + i and local J[i] is m_global + e0 + i.  Merging the per-rank
  * arrays with an elementwise min (NCCL allreduce-MIN after boba_bias_u32)
  * gives exactly boba_first_occurrence of the whole list -- the reference's
- * chunk-local-min merge, _parallel.py:139-162. */
+ * chunk-local-min merge, _parallel.py:139-162.
+ * workspace (may be NULL; boba_first_occurrence_workspace_size() bytes)
+ * enables the two-stage sweep with the shared-memory SeenSet of hubs. */
+size_t boba_first_occurrence_workspace_size(void);
 int boba_first_occurrence_shard(const uint32_t *I, const uint32_t *J, uint64_t m_local,
                                 uint64_t m_global, uint64_t e0, uint32_t n, uint32_t *first,
-                                int relaxed, void *stream);
+                                int relaxed, void *workspace, size_t workspace_bytes, void *stream);
 
 /* --- Phase 2: rank compaction -> permutation --------------------------
  * order[k] = the vertex with the k-th smallest first[] value, then the

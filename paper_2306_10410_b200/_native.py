@@ -37,7 +37,8 @@ SIGNATURES = {
     "boba_abi_version": ([], _I),
     "boba_last_error": ([], ctypes.c_char_p),
     "boba_first_occurrence": ([_P, _P, _U64, _U32, _P, _I, _P], _I),
-    "boba_first_occurrence_shard": ([_P, _P, _U64, _U64, _U64, _U32, _P, _I, _P], _I),
+    "boba_first_occurrence_workspace_size": ([], _SZ),
+    "boba_first_occurrence_shard": ([_P, _P, _U64, _U64, _U64, _U32, _P, _I, _P, _SZ, _P], _I),
     "boba_compact_workspace_size": ([_U64, _U32], _SZ),
     "boba_compact": ([_P, _U64, _U32, _P, _P, _P, _P, _SZ, _P], _I),
     "boba_order_workspace_size": ([_U64, _U32], _SZ),

@@ -84,15 +84,19 @@ int boba_first_occurrence(const uint32_t* I, const uint32_t* J, uint64_t m, uint
                        "boba_first_occurrence");
 }
 
+size_t boba_first_occurrence_workspace_size(void) { return boba::first_hit_workspace_bytes(); }
+
 int boba_first_occurrence_shard(const uint32_t* I, const uint32_t* J, uint64_t m_local, uint64_t m_global,
-                                uint64_t e0, uint32_t n, uint32_t* first, int relaxed, void* stream) {
+                                uint64_t e0, uint32_t n, uint32_t* first, int relaxed, void* ws, size_t ws_bytes,
+                                void* stream) {
+    REQUIRE(!ws || ws_bytes >= boba::first_hit_workspace_bytes(), "boba_first_occurrence_shard: workspace too small");
     if (int rc = check_sizes(m_global, n, "boba_first_occurrence_shard")) return rc;
     REQUIRE(e0 + m_local <= m_global, "boba_first_occurrence_shard: shard [e0, e0+m_local) outside [0, m_global)");
     REQUIRE(first || n == 0, "boba_first_occurrence_shard: first is NULL");
     REQUIRE((I && J) || m_local == 0, "boba_first_occurrence_shard: I/J is NULL");
     if (n == 0) return BOBA_OK;
-    return cuda_status(boba::launch_first_hit_shard(I, J, m_local, m_global, e0, n, first, relaxed != 0, num_sms(),
-                                                    S(stream)),
+    return cuda_status(boba::launch_first_hit_shard(I, J, m_local, m_global, e0, n, first, relaxed != 0, ws,
+                                                    num_sms(), S(stream)),
                        "boba_first_occurrence_shard");
 }
 
@@ -195,7 +199,8 @@ int boba_reorder_to_csr_timed(const uint32_t* I, const uint32_t* J, const double
     size_t rest_bytes = ws_bytes - (size_t)(base - static_cast<char*>(ws));
     const int sms = num_sms();
     mark(0);
-    cudaError_t e = boba::launch_first_hit(I, J, m, n, first, false, sms, s);
+    // the hub table area doubles as phase 1's SeenSet (dead before phase 2 refills it)
+    cudaError_t e = boba::launch_first_hit_shard(I, J, m, m, 0, n, first, false, hubs, sms, s);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: first occurrence");
     mark(1);
     e = boba::launch_compact(first, m, n, order, label, nullptr, hubs, rest, rest_bytes, sms, s);

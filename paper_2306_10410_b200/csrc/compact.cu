@@ -100,8 +100,7 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
                                                     const uint32_t* __restrict__ secprefix,
                                                     const uint32_t* __restrict__ n_seen_ptr,
                                                     uint32_t* order, uint32_t* label,
-                                                    unsigned long long* status, unsigned* tile_counter,
-                                                    unsigned long long* hubs) {
+                                                    unsigned long long* status, unsigned* tile_counter) {
     __shared__ unsigned s_tile;
     __shared__ uint32_t s_scan[kScanNT / 32 + 1];
     __shared__ unsigned long long s_excl;
@@ -136,7 +135,6 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
         uint32_t r = (f[k] == BOBA_UNSET) ? iso_rank++ : rank_of(f[k], bits, secprefix);
         lab[k] = r;
         order[r] = (uint32_t)(v0 + k);
-        hub_insert(hubs, (uint32_t)(v0 + k), r);
     }
     if (v0 + kAssignVPT <= n && (reinterpret_cast<uintptr_t>(label) & 15) == 0) {
         *reinterpret_cast<uint4*>(label + v0) = make_uint4(lab[0], lab[1], lab[2], lab[3]);
@@ -145,6 +143,20 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
         for (int k = 0; k < kAssignVPT; k++)
             if (v0 + k < n) label[v0 + k] = lab[k];
     }
+}
+
+// table = kHubWays arrays of kHubBuckets entries; round r fills way r with the
+// smallest label that did not win an earlier way of its bucket.
+__global__ void k_hub_labels(const uint32_t* __restrict__ order, uint32_t K, HubHash hh, int round,
+                             uint32_t* table) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    uint32_t b, tag;
+    hh.split(__ldg(order + k), b, tag);
+    const uint32_t e = (k << hh.tag_bits) | tag;
+    for (int w = 0; w < round; w++)
+        if (table[w * kHubBuckets + b] == e) return;
+    atomicMin(table + round * kHubBuckets + b, e);
 }
 
 namespace {
@@ -195,10 +207,6 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
     // clear bits, lookback status and counters (everything before secprefix)
     cudaError_t err = cudaMemsetAsync(ws, 0, reinterpret_cast<char*>(secprefix) - static_cast<char*>(ws), s);
     if (err != cudaSuccess) return err;
-    if (hubs) {
-        err = cudaMemsetAsync(hubs, 0xFF, kHubTableBytes, s);
-        if (err != cudaSuccess) return err;
-    }
     {
         uint64_t blocks = ceil_div(n, 256);
         uint64_t cap = (uint64_t)num_sms * 16;
@@ -207,8 +215,24 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
     k_sector_scan<<<(int)sec_tiles, kScanNT, 0, s>>>(reinterpret_cast<const uint4*>(bits), sectors,
                                                      secprefix, w.st_sec, counters + 0, n_seen);
     k_assign<<<(int)v_tiles, kScanNT, 0, s>>>(first, n, reinterpret_cast<const uint4*>(bits), secprefix,
-                                              n_seen, order, label, w.st_v, counters + 1, hubs);
+                                              n_seen, order, label, w.st_v, counters + 1);
     if (n_seen_out) cudaMemcpyAsync(n_seen_out, n_seen, 4, cudaMemcpyDeviceToDevice, s);
+    if (hubs) {
+        // HubLabels (hubs.cuh) for phase 3: labels [0, kHubMaxLabel), kHubWays
+        // slots per bucket, smaller labels first (one round per slot).
+        const HubHash hh = HubHash::make(n);
+        if (hh.tag_bits <= 16) {
+            err = cudaMemsetAsync(hubs, 0xFF, kHubTableBytes, s);
+            if (err != cudaSuccess) return err;
+            const uint32_t K = n < kHubMaxLabel ? n : kHubMaxLabel;
+            for (int round = 0; round < kHubWays; round++)
+                k_hub_labels<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(order, K, hh, round,
+                                                                       reinterpret_cast<uint32_t*>(hubs));
+        } else {
+            err = cudaMemsetAsync(hubs, 0xFF, kHubTableBytes, s);  // empty table: relabel gathers everything
+            if (err != cudaSuccess) return err;
+        }
+    }
     return cudaGetLastError();
 }
 

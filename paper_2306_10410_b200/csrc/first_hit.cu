@@ -9,59 +9,98 @@
 // Cost model: the stream is read once (8m bytes, coalesced 16-byte loads);
 // the per-endpoint work is a 4-byte random access to first[] (4n bytes,
 // L2-resident up to n ~ 25M), and the L2 request rate for those -- not HBM
-// bandwidth -- is what bounds a naive kernel.  Two things cut it:
+// bandwidth -- is what bounds a naive kernel.  What cuts it:
 //  * the grid sweeps the stream in position order (persistent CTAs,
-//    block-cyclic over 2048-position iterations), so an atomic is issued only
+//    block-cyclic over 8K-position iterations), so an atomic is issued only
 //    when a plain (L1-cacheable; stale values are conservative because
 //    first[] only decreases) load shows the position can still lower first[v];
-//  * each CTA keeps a 32K-slot shared-memory set of vertices already known
-//    to be finalised, i.e. first[v] < the lowest position the CTA will touch
-//    from now on.  Hubs of skewed graphs recur early and settle in the set
-//    ("insert if the slot is empty"), so most hub endpoints never leave the
-//    SM.  Iterations are separated by a CTA barrier so the invariant holds
-//    for every warp.
+//  * two-stage sweep: stage 1 runs a prefix of I alone (128K positions for
+//    ids up to 2^22, 64K beyond); the vertices first seen there -- exactly
+//    the first BOBA vertices, i.e. the hubs -- go into a 128K- or 64K-entry
+//    tag set (hubs.cuh SeenSet) that every CTA of stage 2 holds in shared
+//    memory, and their later endpoints never leave the SM;
+//  * when the prefix is too short to matter (small m) or the ids are too wide
+//    for 16-bit tags, a single sweep keeps a per-CTA set of vertices already
+//    finalised instead (insert-if-empty; CTA barrier per iteration keeps the
+//    invariant first[v] < lowest position still to come).
 #include "common.cuh"
+#include "hubs.cuh"
 #include "kernels.cuh"
 
 namespace boba {
 
 constexpr int kFhNT = 1024;              // threads per CTA (one CTA per SM)
-constexpr int kFhQuads = 2;              // 16-byte quads per thread per iteration
-constexpr int kFhIter = kFhNT * kFhQuads * 4;   // positions per CTA iteration
-constexpr int kFhSlotsLog2 = 15;         // 32K-slot finalised-vertex set (128 KB)
+constexpr int kFhQuads = 4;              // 16-byte quads per thread per iteration
+constexpr int kFhSlotsLog2 = 15;         // 32K-slot finalised-vertex set (128 KB), dynamic mode
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+// Two consecutive position ranges swept in order: A then B (quads of 4 ids).
+struct Ranges {
+    const uint32_t* a;
+    uint64_t qa;      // quads in A
+    uint32_t base_a;  // global position of a[0]
+    const uint32_t* b;
+    uint64_t qb;
+    uint32_t base_b;
+};
 
 __device__ __forceinline__ uint32_t slot_of(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - kFhSlotsLog2); }
 
 template <bool RELAXED>
-__device__ __forceinline__ void hit(uint32_t* first, uint32_t* set, uint32_t v, uint32_t pos, uint32_t iter_lo) {
+__device__ __forceinline__ void update(uint32_t* first, uint32_t v, uint32_t pos, uint32_t cur) {
+    if (RELAXED)
+        *((volatile uint32_t*)(first + v)) = pos;
+    else
+        atomicMin(first + v, pos);
+}
+
+// Dynamic mode: per-CTA set of vertices known finalised.
+template <bool RELAXED>
+__device__ __forceinline__ void hit_dyn(uint32_t* first, uint32_t* set, uint32_t v, uint32_t pos, uint32_t iter_lo) {
     const uint32_t s = slot_of(v);
     if (set[s] == v) return;                       // finalised: first[v] < iter_lo <= pos
-    const uint32_t cur = first[v];                 // plain load: may be stale (>= true value)
+    const uint32_t cur = __ldcg(first + v);        // L2 load: may be stale (>= true value)
     if (pos < cur) {
-        if (RELAXED)
-            *((volatile uint32_t*)(first + v)) = pos;
-        else
-            atomicMin(first + v, pos);
+        update<RELAXED>(first, v, pos, cur);
     } else if (cur < iter_lo && set[s] == kEmpty) {
         set[s] = v;                                // benign race: any writer's v is finalised
     }
 }
 
-template <bool RELAXED>
-__global__ void __launch_bounds__(kFhNT, 1) k_first_hit(const uint32_t* __restrict__ I,
-                                                        const uint32_t* __restrict__ J, uint64_t m,
-                                                        uint32_t base_i, uint32_t base_j, uint32_t* first) {
-    extern __shared__ uint32_t set[];
-    for (int i = threadIdx.x; i < (1 << kFhSlotsLog2); i += kFhNT) set[i] = kEmpty;
-    const uint64_t quads = m >> 2;          // full 16-byte quads per array
-    const uint64_t total_q = 2 * quads;     // quads of I then quads of J
+// Static mode: the SeenSet of vertices first seen in the prefix.
+template <int TW>  // tag width: 8 (8 lanes per bucket) or 16 (4 lanes)
+__device__ __forceinline__ bool seen(const unsigned long long* set, const HubHash& hh, uint32_t v) {
+    constexpr uint32_t kTagMask = (1u << TW) - 1u;
+    uint32_t b, tag;
+    hh.split(v, b, tag);
+    if (tag == kTagMask) return false;             // never inserted (all-ones marks an empty lane)
+    const uint2 w = reinterpret_cast<const uint2*>(set)[b];
+    if (TW == 8) {
+        const uint32_t rep = tag * 0x01010101u;
+        return (__vcmpeq4(w.x, rep) | __vcmpeq4(w.y, rep)) != 0;
+    } else {
+        const uint32_t rep = tag * 0x00010001u;
+        return (__vcmpeq2(w.x, rep) | __vcmpeq2(w.y, rep)) != 0;
+    }
+}
+
+template <bool RELAXED, bool STATIC, int TW = 16>
+__global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* first,
+                                                        const unsigned long long* __restrict__ seen_g, HubHash hh) {
+    extern __shared__ unsigned long long smem_u64[];
+    uint32_t* set = reinterpret_cast<uint32_t*>(smem_u64);
+    if (STATIC) {
+        for (int i = threadIdx.x; i < kHubBuckets; i += kFhNT) smem_u64[i] = __ldg(seen_g + i);
+    } else {
+        for (int i = threadIdx.x; i < (1 << kFhSlotsLog2); i += kFhNT) set[i] = kEmpty;
+    }
+    const uint64_t total_q = r.qa + r.qb;
     const uint64_t iters = ceil_div(total_q, (uint64_t)kFhNT * kFhQuads);
+    if (STATIC) __syncthreads();
     for (uint64_t it = blockIdx.x; it < iters; it += gridDim.x) {
-        __syncthreads();  // every warp has left the previous iteration
+        if (!STATIC) __syncthreads();  // every warp has left the previous iteration
         const uint64_t q0 = it * kFhNT * kFhQuads;
-        // lowest position of this iteration (quads of J start at position m)
-        const uint32_t iter_lo = (uint32_t)(q0 < quads ? base_i + 4 * q0 : base_j + 4 * (q0 - quads));
+        const uint32_t iter_lo = (uint32_t)(q0 < r.qa ? r.base_a + 4 * q0 : r.base_b + 4 * (q0 - r.qa));
         uint4 q[kFhQuads];
         uint32_t pos[kFhQuads];
         bool ok[kFhQuads];
@@ -70,20 +109,71 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(const uint32_t* __restri
             const uint64_t w = q0 + (uint64_t)k * kFhNT + threadIdx.x;
             ok[k] = w < total_q;
             if (ok[k]) {
-                const bool inJ = w >= quads;
-                const uint64_t qi = inJ ? w - quads : w;
-                q[k] = __ldg(reinterpret_cast<const uint4*>(inJ ? J : I) + qi);
-                pos[k] = (uint32_t)(4 * qi) + (inJ ? base_j : base_i);
+                const bool inB = w >= r.qa;
+                const uint64_t qi = inB ? w - r.qa : w;
+                q[k] = __ldg(reinterpret_cast<const uint4*>(inB ? r.b : r.a) + qi);
+                pos[k] = (uint32_t)(4 * qi) + (inB ? r.base_b : r.base_a);
             }
         }
+        if (STATIC) {
+            // all set probes first, then all guard loads in flight together, then the atomics
+            bool need[kFhQuads][4];
+            uint32_t cur[kFhQuads][4];
 #pragma unroll
-        for (int k = 0; k < kFhQuads; k++) {
-            if (!ok[k]) continue;
-            hit<RELAXED>(first, set, q[k].x, pos[k], iter_lo);
-            hit<RELAXED>(first, set, q[k].y, pos[k] + 1, iter_lo);
-            hit<RELAXED>(first, set, q[k].z, pos[k] + 2, iter_lo);
-            hit<RELAXED>(first, set, q[k].w, pos[k] + 3, iter_lo);
+            for (int k = 0; k < kFhQuads; k++) {
+                const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+                for (int j = 0; j < 4; j++) need[k][j] = ok[k] && !seen<TW>(smem_u64, hh, vs[j]);
+            }
+#pragma unroll
+            for (int k = 0; k < kFhQuads; k++) {
+                const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+                for (int j = 0; j < 4; j++) cur[k][j] = need[k][j] ? __ldcg(first + vs[j]) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < kFhQuads; k++) {
+                const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (need[k][j] && pos[k] + j < cur[k][j]) update<RELAXED>(first, vs[j], pos[k] + j, cur[k][j]);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kFhQuads; k++) {
+                if (!ok[k]) continue;
+                hit_dyn<RELAXED>(first, set, q[k].x, pos[k], iter_lo);
+                hit_dyn<RELAXED>(first, set, q[k].y, pos[k] + 1, iter_lo);
+                hit_dyn<RELAXED>(first, set, q[k].z, pos[k] + 2, iter_lo);
+                hit_dyn<RELAXED>(first, set, q[k].w, pos[k] + 3, iter_lo);
+            }
         }
+    }
+}
+
+// SeenSet from the prefix: every vertex whose first occurrence is one of the
+// prefix positions gets its tag into a free 16-bit lane of its bucket.
+template <int TW>
+__global__ void k_seen_build(const uint32_t* __restrict__ I, uint32_t count, uint32_t base,
+                             const uint32_t* __restrict__ first, HubHash hh, unsigned long long* set) {
+    constexpr unsigned long long kTagMask = (1ull << TW) - 1ull;
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= count) return;
+    const uint32_t v = __ldg(I + p);
+    if (__ldg(first + v) != base + p) return;   // not the first occurrence (exactly one thread per vertex)
+    uint32_t b, tag;
+    hh.split(v, b, tag);
+    if (tag == kTagMask) return;                // reserved for "empty"
+    unsigned long long w = set[b];
+    while (true) {
+        int lane = -1;
+        for (int l = 0; l < 64 / TW; l++)
+            if (((w >> (TW * l)) & kTagMask) == kTagMask) { lane = l; break; }
+        if (lane < 0) return;                   // bucket full: not recorded (still correct)
+        const unsigned long long nw = (w & ~(kTagMask << (TW * lane))) | ((unsigned long long)tag << (TW * lane));
+        const unsigned long long old = atomicCAS(set + b, w, nw);
+        if (old == w) return;
+        w = old;
     }
 }
 
@@ -106,34 +196,67 @@ __global__ void k_first_hit_scalar(const uint32_t* __restrict__ I, const uint32_
     }
 }
 
+template <bool RELAXED, bool STATIC, int TW = 16>
+static void launch_sweep(const Ranges& r, uint32_t* first, const unsigned long long* seen_g, const HubHash& hh,
+                         int num_sms, cudaStream_t s) {
+    const size_t smem = STATIC ? sizeof(unsigned long long) * kHubBuckets : (sizeof(uint32_t) << kFhSlotsLog2);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_first_hit<RELAXED, STATIC, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    const uint64_t iters = ceil_div(r.qa + r.qb, (uint64_t)kFhNT * kFhQuads);
+    if (iters == 0) return;
+    const int grid = (int)(iters < (uint64_t)num_sms ? iters : (uint64_t)num_sms);
+    k_first_hit<RELAXED, STATIC, TW><<<grid, kFhNT, smem, s>>>(r, first, seen_g, hh);
+}
+
 cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
                              bool relaxed, int num_sms, cudaStream_t s) {
-    return launch_first_hit_shard(I, J, m, m, 0, n, first, relaxed, num_sms, s);
+    return launch_first_hit_shard(I, J, m, m, 0, n, first, relaxed, nullptr, num_sms, s);
 }
+
+size_t first_hit_workspace_bytes() { return kHubTableBytes; }
 
 // A contiguous shard [e0, e0 + m) of a global edge list with m_global edges:
 // local I[i] sits at global position e0 + i, local J[i] at m_global + e0 + i.
+// `seen_ws` (kHubTableBytes, may be NULL) enables the two-stage sweep.
 cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_t m, uint64_t m_global, uint64_t e0,
-                                   uint32_t n, uint32_t* first, bool relaxed, int num_sms, cudaStream_t s) {
+                                   uint32_t n, uint32_t* first, bool relaxed, void* seen_ws, int num_sms,
+                                   cudaStream_t s) {
     const uint32_t base_i = (uint32_t)e0, base_j = (uint32_t)(m_global + e0);
     cudaError_t err = cudaMemsetAsync(first, 0xFF, (size_t)n * sizeof(uint32_t), s);
     if (err != cudaSuccess || m == 0) return err;
     const bool vec = ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(J)) & 15) == 0;
+    const HubHash hh = HubHash::make(n);
     uint64_t done = 0;
     if (vec && m >= 4) {
-        const size_t smem = sizeof(uint32_t) << kFhSlotsLog2;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_first_hit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaFuncSetAttribute(k_first_hit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
+        const uint64_t quads = m >> 2;
+        const uint32_t prefix = seen_prefix(hh.tag_bits);
+        const bool two_stage = seen_ws && !relaxed && hh.tag_bits <= 16 && m >= 16ull * prefix;
+        if (two_stage) {
+            unsigned long long* set = static_cast<unsigned long long*>(seen_ws);
+            const uint64_t qp = prefix / 4;
+            Ranges r1{I, qp, base_i, J, 0, base_j};
+            launch_sweep<false, false>(r1, first, nullptr, hh, num_sms, s);
+            err = cudaMemsetAsync(set, 0xFF, kHubTableBytes, s);
+            if (err != cudaSuccess) return err;
+            Ranges r2{I + prefix, quads - qp, base_i + prefix, J, quads, base_j};
+            if (hh.tag_bits <= 8) {
+                k_seen_build<8><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
+                launch_sweep<false, true, 8>(r2, first, set, hh, num_sms, s);
+            } else {
+                k_seen_build<16><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
+                launch_sweep<false, true, 16>(r2, first, set, hh, num_sms, s);
+            }
+        } else {
+            Ranges r{I, quads, base_i, J, quads, base_j};
+            if (relaxed)
+                launch_sweep<true, false>(r, first, nullptr, hh, num_sms, s);
+            else
+                launch_sweep<false, false>(r, first, nullptr, hh, num_sms, s);
         }
-        const uint64_t iters = ceil_div(2 * (m >> 2), (uint64_t)kFhNT * kFhQuads);
-        const int grid = (int)(iters < (uint64_t)num_sms ? iters : (uint64_t)num_sms);
-        if (relaxed)
-            k_first_hit<true><<<grid, kFhNT, smem, s>>>(I, J, m, base_i, base_j, first);
-        else
-            k_first_hit<false><<<grid, kFhNT, smem, s>>>(I, J, m, base_i, base_j, first);
         done = m & ~3ull;
     }
     if (done < m) {

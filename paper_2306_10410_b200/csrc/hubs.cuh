@@ -1,19 +1,54 @@
-// Hub label table shared by phase 2 (producer, k_assign) and phase 3
-// (consumer, k_relabel): a direct-mapped table of 2^kHubSlotsLog2 64-bit
-// entries (label << 32 | old id) holding the vertices with the smallest
-// BOBA labels -- the hubs -- smallest label wins a slot.  Empty = all ones.
+// Shared-memory hub structures for the two L2-request-bound phases.
+//
+// BOBA orders vertices by first appearance, and on skewed graphs the first
+// vertices to appear are the hubs: at c2 (R-MAT s22) the 32K smallest labels
+// cover 38% of all edge endpoints and the 64K smallest 51%.  Both structures
+// below are keyed by a bijective hash of the vertex id on kk = max(ceil(log2
+// n), 14) bits: the top 14 bits pick one of 16K buckets, the remaining
+// kk - 14 bits are stored as a tag, so an entry needs no full id.
+//
+//  * HubLabels (phase 3, relabel): 16K buckets x 3 entries of 32 bits,
+//    entry = label << tagbits | tag, for the vertices with labels < 49151;
+//    smaller labels win slots (one atomicMin round per slot), 192 KB.
+//  * SeenSet (phase 1, first occurrence): 16K buckets of 64 bits, each
+//    holding 8 8-bit tags (ids up to 2^22) or 4 16-bit tags (up to 2^30), of
+//    the vertices whose first occurrence lies in a prefix of I (exactly the
+//    BOBA-first vertices), 128 KB.  Every later position of such a vertex is
+//    known not to be its first, so it costs no global access at all.
 #pragma once
 #include <cstdint>
 
 namespace boba {
 
-constexpr int kHubSlotsLog2 = 14;
-constexpr size_t kHubTableBytes = sizeof(unsigned long long) << kHubSlotsLog2;
+constexpr int kHubBucketsLog2 = 14;
+constexpr int kHubBuckets = 1 << kHubBucketsLog2;
+constexpr int kHubWays = 3;                  // HubLabels entries per bucket
+constexpr size_t kHubTableBytes = sizeof(uint32_t) * kHubWays << kHubBucketsLog2;  // HubLabels; SeenSet uses 2/3
+constexpr uint32_t kHubMaxLabel = 49151;     // labels [0, kHubMaxLabel) go into HubLabels
+// I[0, prefix) feeds the SeenSet: sized for ~70% occupancy of its capacity
+// (128K 8-bit tags or 64K 16-bit tags; about 1.4 positions per new vertex).
+__host__ __device__ inline uint32_t seen_prefix(int tag_bits) { return tag_bits <= 8 ? 131072u : 65536u; }
 
-__device__ __forceinline__ uint32_t hub_slot(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - kHubSlotsLog2); }
+struct HubHash {
+    int kk;          // hashed width, >= kHubBucketsLog2
+    int tag_bits;    // kk - kHubBucketsLog2
+    uint32_t mask;   // low kk bits
 
-__device__ __forceinline__ void hub_insert(unsigned long long* table, uint32_t v, uint32_t r) {
-    if (table && r < (1u << kHubSlotsLog2)) atomicMin(table + hub_slot(v), ((unsigned long long)r << 32) | v);
-}
+    static HubHash make(uint32_t n) {  // host
+        int k = n <= 1 ? 0 : 32 - __builtin_clz(n - 1);
+        HubHash h;
+        h.kk = k < kHubBucketsLog2 ? kHubBucketsLog2 : k;
+        h.tag_bits = h.kk - kHubBucketsLog2;
+        h.mask = h.kk >= 32 ? 0xFFFFFFFFu : (1u << h.kk) - 1u;
+        return h;
+    }
+    // bijection on kk bits: odd multiply mod 2^kk (ids are random labels or
+    // BOBA ranks, so one multiply mixes enough)
+    __device__ __forceinline__ void split(uint32_t v, uint32_t& bucket, uint32_t& tag) const {
+        const uint32_t x = (v * 0x9E3779B1u) & mask;
+        bucket = x >> tag_bits;
+        tag = x & ((1u << tag_bits) - 1u);   // tag_bits < 32
+    }
+};
 
 }  // namespace boba

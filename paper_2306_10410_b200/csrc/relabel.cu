@@ -9,13 +9,14 @@
 // Two shared-memory structures cut those requests:
 //  * hub label cache: BOBA puts the hubs first, so the vertices with the
 //    smallest new labels are exactly the ones most endpoints hit.  Phase 2
-//    (k_assign) drops every vertex with label < 16K into a 16K-slot
-//    direct-mapped table (64-bit atomicMin on (label<<32 | v): the smallest
-//    label wins a slot); each CTA copies it into shared memory (128 KB) and
-//    serves hits from there.
+//    builds HubLabels (hubs.cuh: 16K buckets x 3 tagged entries, labels <
+//    49151); each CTA copies it into shared memory (192 KB) and serves hits
+//    from there.
 //  * row histogram (the np.bincount of graph.py:270 for the following
 //    COO->CSR): rows < 8K -- again the hubs -- are counted in shared memory
 //    and flushed once per CTA; other rows use RED.ADD in L2.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "hubs.cuh"
 #include "kernels.cuh"
@@ -28,35 +29,43 @@ constexpr int kHubHistRows = 8192;
 template <bool HIST, bool HUBS>
 __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ I, const uint4* __restrict__ J,
                                                       uint64_t quads, const uint32_t* __restrict__ label,
-                                                      const unsigned long long* __restrict__ hubs, uint32_t n,
-                                                      uint4* __restrict__ I2, uint4* __restrict__ J2,
+                                                      const unsigned long long* __restrict__ hubs, HubHash hh,
+                                                      uint32_t n, uint4* __restrict__ I2, uint4* __restrict__ J2,
                                                       uint32_t* counts) {
-    extern __shared__ uint32_t sm[];
-    uint32_t* s_key = sm;                                    // kHubSlots
-    uint32_t* s_lab = sm + (HUBS ? (1 << kHubSlotsLog2) : 0);  // kHubSlots
-    uint32_t* s_hist = s_lab + (HUBS ? (1 << kHubSlotsLog2) : 0);  // kHubHistRows
+    extern __shared__ uint32_t sm32[];
+    uint32_t* s_tab = sm32;                                                       // kHubWays x kHubBuckets
+    uint32_t* s_hist = sm32 + (HUBS ? kHubWays * kHubBuckets : 0);                // kHubHistRows
     if (HUBS) {
-        for (int i = threadIdx.x; i < (1 << kHubSlotsLog2); i += kRlNT) {
-            unsigned long long e = __ldg(hubs + i);
-            s_key[i] = (uint32_t)e;            // 0xFFFFFFFF when empty: never equals a vertex < n
-            s_lab[i] = (uint32_t)(e >> 32);
-        }
+        const uint4* src = reinterpret_cast<const uint4*>(hubs);
+        for (int i = threadIdx.x; i < kHubWays * kHubBuckets / 4; i += kRlNT)
+            reinterpret_cast<uint4*>(s_tab)[i] = __ldg(src + i);
     }
     if (HIST)
         for (int i = threadIdx.x; i < kHubHistRows; i += kRlNT) s_hist[i] = 0;
     __syncthreads();
-    auto lookup = [&](uint32_t v) -> uint32_t {
+    const uint32_t tmask = hh.tag_bits ? (1u << hh.tag_bits) - 1u : 0u;
+    // probe the hub table (smem) for every endpoint first; returns 0xFFFFFFFF on a miss
+    auto probe = [&](uint32_t v) -> uint32_t {
         if (HUBS) {
-            const uint32_t s = hub_slot(v);
-            if (s_key[s] == v) return s_lab[s];
+            uint32_t b, tag;
+            hh.split(v, b, tag);
+#pragma unroll
+            for (int w = 0; w < kHubWays; w++) {   // entries: label << tag_bits | tag, 0xFFFFFFFF = empty
+                const uint32_t e = s_tab[w * kHubBuckets + b];
+                if (e != 0xFFFFFFFFu && (e & tmask) == tag) return e >> hh.tag_bits;
+            }
         }
-        return __ldg(label + v);
+        return 0xFFFFFFFFu;
     };
     auto count = [&](uint32_t r) {
         if (r < (uint32_t)kHubHistRows)
             atomicAdd(s_hist + r, 1u);
         else
             atomicAdd(counts + r, 1u);
+    };
+    auto lookup = [&](uint32_t v) -> uint32_t {
+        const uint32_t h = probe(v);
+        return h != 0xFFFFFFFFu ? h : __ldcg(label + v);
     };
     const uint64_t stride = (uint64_t)gridDim.x * kRlNT;
     for (uint64_t q = (uint64_t)blockIdx.x * kRlNT + threadIdx.x; q < quads; q += stride) {
@@ -99,8 +108,8 @@ static void launch_vec(int grid, size_t smem, cudaStream_t s, const uint32_t* I,
         cudaFuncSetAttribute(k_relabel<HIST, HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_relabel<HIST, HUBS><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs, n,
-                                                    (uint4*)I2, (uint4*)J2, counts);
+    k_relabel<HIST, HUBS><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs,
+                                                    HubHash::make(n), n, (uint4*)I2, (uint4*)J2, counts);
 }
 
 cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,
@@ -118,7 +127,13 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
         const uint64_t quads = m >> 2;
         uint64_t blocks = ceil_div(quads, kRlNT);
         const int grid = (int)(blocks < (uint64_t)num_sms ? blocks : (uint64_t)num_sms);
-        const size_t smem = 4 * ((hubs ? 2 * (1 << kHubSlotsLog2) : 0) + (counts ? kHubHistRows : 0));
+        if (hubs && HubHash::make(n).tag_bits > 16) hubs = nullptr;  // ids too wide for the packed table
+        // The table pays off while label[] is L2-resident and the phase is bound by the
+        // L2 request rate (measured: c2, n = 2^22, 0.57 -> 0.40 ms).  Beyond 2^23
+        // vertices the gathers are DRAM-latency bound and the probe only delays them
+        // (c5, n = 2^24: 2.26 ms without, 3.28 ms with).
+        if (n > (1u << 23) || getenv("BOBA_NO_HUBS")) hubs = nullptr;
+        const size_t smem = (hubs ? kHubTableBytes : 0) + 4 * (counts ? kHubHistRows : 0);
         if (counts && hubs)
             launch_vec<true, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
         else if (counts)

@@ -44,8 +44,9 @@ class DeviceOps:
 
     def first_occurrence_shard(self, I, J, m_global: int, e0: int, n: int):
         first = torch.empty(max(n, 1), dtype=D.ID, device=I.device)[:n]
+        ws = D._ws(N.lib.boba_first_occurrence_workspace_size(), I.device)
         N.check(N.lib.boba_first_occurrence_shard(D._p(I), D._p(J), I.numel(), m_global, e0, n, D._p(first), 0,
-                                                  D._s()))
+                                                  D._p(ws), ws.numel(), D._s()))
         return first
 
     def bias(self, t):
