@@ -43,7 +43,9 @@ struct RadixCfg {
     static constexpr int NW = NT / 32;
     static constexpr int TILE = NT * IPT;
     static constexpr int BPT = B >= NT ? B / NT : 1;              // digits per thread in the scans
-    static constexpr int HIST_BYTES = (NW * B * 2 + 15) / 16 * 16;  // 16-bit warp counters
+    static constexpr int SUB = 1;  // measured: 2 or 4 chains cost more in registers than they gain  // independent counter chains per warp
+    static constexpr int VW = NW * SUB;                              // "virtual warps" (warp, chain)
+    static constexpr int HIST_BYTES = (VW * B * 2 + 15) / 16 * 16;  // 16-bit counters per virtual warp
     static constexpr int STAGE_BYTES = TILE * 8;                    // staged keys + payloads
     static constexpr int RAW_BYTES = TILE * 4;                      // payloads prefetched by cp.async
     static constexpr size_t SMEM = (size_t)HIST_BYTES + STAGE_BYTES + RAW_BYTES + 2 * B * 4;  // + s_off, s_glob
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     const uint64_t wslot = tile_base + (uint64_t)warp * 32 * IPT;
     const bool full = tile_base + TILE <= m;
 
-    for (int i = threadIdx.x; i < NW * B / 2; i += NT) reinterpret_cast<uint32_t*>(s_hist)[i] = 0;
+    for (int i = threadIdx.x; i < C::VW * B / 2; i += NT) reinterpret_cast<uint32_t*>(s_hist)[i] = 0;
     // Prefetch this warp's payload run (IPT*32 words) into shared memory with
     // cp.async; it lands while the warp ranks its keys.
     uint32_t* wraw = s_raw + warp * 32 * IPT;
@@ -183,35 +185,44 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
         }
     }
     __syncthreads();
-    uint16_t* wh = s_hist + warp * B;
+    // A warp's IPT slots form SUB independent chains of consecutive slots, each
+    // with its own counters (a "virtual warp"), so SUB read-modify-write chains
+    // through shared memory proceed in parallel.
+    constexpr int SUB = C::SUB, SPC = IPT / SUB;
+    uint16_t* wh = s_hist + warp * SUB * B;
     const unsigned lt = lanemask_lt();
 #pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const bool ok = full || wslot + (uint64_t)i * 32 + lane < m;
-        const uint32_t d = op(key[i]);
-        unsigned peers = full ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, ok);
-        // peers &= lanes whose digit bit b equals mine, for every bit b:
-        // one predicate test, one ballot and one predicated AND per bit.
+    for (int si = 0; si < SPC; si++) {
 #pragma unroll
-        for (int b = 0; b < RB; b++) {  // bits >= `bits` are zero in every lane: no effect
-            asm("{\n\t"
-                ".reg .pred p;\n\t"
-                ".reg .b32 bb;\n\t"
-                "and.b32 bb, %1, %2;\n\t"
-                "setp.ne.u32 p, bb, 0;\n\t"
-                "vote.sync.ballot.b32 bb, p, 0xffffffff;\n\t"
-                "@!p not.b32 bb, bb;\n\t"
-                "and.b32 %0, %0, bb;\n\t"
-                "}"
-                : "+r"(peers)
-                : "r"(d), "r"(1u << b));
+        for (int c = 0; c < SUB; c++) {
+            const int i = c * SPC + si;
+            const bool ok = full || wslot + (uint64_t)i * 32 + lane < m;
+            const uint32_t d = op(key[i]);
+            unsigned peers = full ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, ok);
+            // peers &= lanes whose digit bit b equals mine, for every bit b:
+            // one predicate test, one ballot and one predicated AND per bit.
+#pragma unroll
+            for (int b = 0; b < RB; b++) {  // bits >= `bits` are zero in every lane: no effect
+                asm("{\n\t"
+                    ".reg .pred p;\n\t"
+                    ".reg .b32 bb;\n\t"
+                    "and.b32 bb, %1, %2;\n\t"
+                    "setp.ne.u32 p, bb, 0;\n\t"
+                    "vote.sync.ballot.b32 bb, p, 0xffffffff;\n\t"
+                    "@!p not.b32 bb, bb;\n\t"
+                    "and.b32 %0, %0, bb;\n\t"
+                    "}"
+                    : "+r"(peers)
+                    : "r"(d), "r"(1u << b));
+            }
+            const unsigned below = peers & lt;
+            uint16_t* ch = wh + c * B;
+            uint32_t pre = 0;
+            if (ok) pre = ch[d];
+            __syncwarp();
+            if (ok && below == 0) ch[d] = (uint16_t)(pre + __popc(peers));
+            rank[i] = ok ? pre + __popc(below) : 0xFFFFFFFFu;
         }
-        const unsigned below = peers & lt;
-        uint32_t pre = 0;
-        if (ok) pre = wh[d];
-        __syncwarp();
-        if (ok && below == 0) wh[d] = (uint16_t)(pre + __popc(peers));
-        rank[i] = ok ? pre + __popc(below) : 0xFFFFFFFFu;
         __syncwarp();
     }
     __syncthreads();
@@ -223,7 +234,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
         uint32_t run = 0;
         if (d < nb) {
 #pragma unroll
-            for (int w = 0; w < NW; w++) {
+            for (int w = 0; w < C::VW; w++) {
                 const uint32_t c = s_hist[w * B + d];
                 s_hist[w * B + d] = (uint16_t)run;
                 run += c;
@@ -252,7 +263,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     for (int i = 0; i < IPT; i++) {
         if (rank[i] != 0xFFFFFFFFu) {
             const uint32_t d = op(key[i]);
-            rank[i] += s_off[d] + wh[d];
+            rank[i] += s_off[d] + wh[(i / SPC) * B + d];
         }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
