@@ -20,12 +20,21 @@
 //     the tails of the CTAs before it from a segmented-scan fix-up over the
 //     per-CTA tails (k_spmv_chunk_agg + k_spmv_carry); no CTA waits on another
 //     and every sum has a fixed association, so y is bitwise deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace boba {
 
 constexpr int kSpNT = 256, kSpIPT = 8, kSpTile = kSpNT * kSpIPT;
+
+// Streaming loads that must not evict the x vector's hot lines from L1.
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 
 template <typename T>
 struct SegValT {
@@ -87,11 +96,26 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
     const uint64_t j0 = d0 - i0, j1 = d1 - i1;
     const uint32_t nrows = (uint32_t)(i1 - i0), nnz = (uint32_t)(j1 - j0);
     for (uint32_t k = threadIdx.x; k <= nrows; k += kSpNT)
-        s_end[k] = (i0 + k < n) ? __ldg(offsets + i0 + 1 + k) : 0xFFFFFFFFu;
-    for (uint32_t k = threadIdx.x; k < nnz; k += kSpNT) {
-        T p = __ldg(x + __ldg(indices + j0 + k));
-        if (w) p *= __ldg(w + j0 + k);
-        s_val[k] = p;
+        s_end[k] = (i0 + k < n) ? ld_stream_u32(offsets + i0 + 1 + k) : 0xFFFFFFFFu;
+    {
+        // all index loads, then all x gathers in flight together (nnz <= kSpTile)
+        uint32_t col[kSpIPT];
+#pragma unroll
+        for (int u = 0; u < kSpIPT; u++) {
+            const uint32_t k = threadIdx.x + u * kSpNT;
+            col[u] = k < nnz ? ld_stream_u32(indices + j0 + k) : 0u;
+        }
+        T p[kSpIPT];
+#pragma unroll
+        for (int u = 0; u < kSpIPT; u++) {
+            const uint32_t k = threadIdx.x + u * kSpNT;
+            p[u] = k < nnz ? __ldg(x + col[u]) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < kSpIPT; u++) {
+            const uint32_t k = threadIdx.x + u * kSpNT;
+            if (k < nnz) s_val[k] = w ? p[u] * __ldg(w + j0 + k) : p[u];
+        }
     }
     __syncthreads();
     // Per-thread sequential fold over kSpIPT merge items.
@@ -279,6 +303,12 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
     T* tile_tail = reinterpret_cast<T*>(p + 2 * arr);
     unsigned* chunk_flag = reinterpret_cast<unsigned*>(p + 3 * arr);
     T* chunk_val = reinterpret_cast<T*>(p + 3 * arr + ((chunks + 1) * 4 + 15) / 16 * 16);
+    static int carve = -2;
+    if (carve == -2) {
+        const char* e = getenv("BOBA_SPMV_CARVEOUT");
+        carve = e ? atoi(e) : -1;
+        if (carve >= 0) cudaFuncSetAttribute(k_spmv_merge<T>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    }
     k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
     k_spmv_merge<T><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail);
     if (tiles > 1) {
