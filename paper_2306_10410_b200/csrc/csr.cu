@@ -70,6 +70,13 @@ __global__ void __launch_bounds__(kOffNT) k_scan_offsets(const uint32_t* __restr
     }
 }
 
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+
+static cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t s) {
+    k_set_u32<<<1, 1, 0, s>>>(p, v);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------- offsets from sorted rows ---
 // Without a row histogram: after the last radix pass the rows are sorted, so
 // offsets[key[g]] = g wherever the key changes (offsets pre-filled with
@@ -260,7 +267,7 @@ CsrWs carve(void* base, uint64_t m, uint32_t n) {
 template <int RB, int NT, int IPT, int MINB, typename Op = DigitShift>
 cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, Op op, int bits, uint32_t* H,
                           unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                          int num_sms, cudaStream_t s) {
+                          int num_sms, cudaStream_t s, uint32_t* row_starts = nullptr, bool skip_up = false) {
     using C = RadixCfg<RB, NT, IPT>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -272,39 +279,50 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
     const uint64_t tiles = ceil_div(m, C::TILE);
     const uint64_t hcount = tiles << bits;
     const uint64_t up_grid = tiles < (uint64_t)num_sms * 8 ? tiles : (uint64_t)num_sms * 8;
-    k_radix_upsweep<RB, NT, IPT, Op><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, op, bits, tiles, H);
+    if (!skip_up) k_radix_upsweep<RB, NT, IPT, Op><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, op, bits, tiles, H);
     cudaError_t e = cudaMemsetAsync(scan_status, 0, (ceil_div(hcount, kScanTile) + 1) * 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 4, s);
     if (e != cudaSuccess) return e;
     k_scan_u32<<<(unsigned)ceil_div(hcount, kScanTile), kScanTileNT, 0, s>>>(H, hcount, 0u, scan_status, counter);
     k_radix_downsweep<RB, NT, IPT, MINB, Op><<<(unsigned)tiles, NT, C::SMEM, s>>>(kin, vin, m, op, bits, tiles, H,
-                                                                                kout, vout);
+                                                                                kout, vout, row_starts);
     return cudaGetLastError();
 }
 
 template <int RB, int NT, int IPT, int MINB>
 cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits, uint32_t* H,
                        unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                       int num_sms, cudaStream_t s) {
+                       int num_sms, cudaStream_t s, uint32_t* row_starts, bool skip_up) {
     return radix_pass_op<RB, NT, IPT, MINB, DigitShift>(kin, vin, m, DigitShift{shift, (1u << bits) - 1u}, bits, H,
-                                                        scan_status, counter, kout, vout, num_sms, s);
+                                                        scan_status, counter, kout, vout, num_sms, s, row_starts,
+                                                        skip_up);
 }
 
 cudaError_t dispatch_pass(Variant v, const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits,
                           uint32_t* H, unsigned long long* st, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                          int sms, cudaStream_t s) {
+                          int sms, cudaStream_t s, uint32_t* row_starts, bool skip_up) {
     switch (v) {
         case Variant::R8x256:
-            return radix_pass<8, 256, 16, 4>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s);
+            return radix_pass<8, 256, 16, 4>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s, row_starts,
+                                             skip_up);
         case Variant::R8x512:
-            return radix_pass<8, 512, 16, 2>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s);
+            return radix_pass<8, 512, 16, 2>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s, row_starts,
+                                             skip_up);
         default:
-            return radix_pass<11, 256, 16, 2>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s);
+            return radix_pass<11, 256, 16, 2>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s,
+                                              row_starts, skip_up);
     }
 }
 }  // namespace
 
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool /*weighted*/) { return carve(nullptr, m, n).total; }
+
+uint32_t* csr_first_pass_hist(void* ws, uint64_t m, uint32_t n, int* dbits) {
+    const CsrPlan p = plan_for(n);
+    if (p.passes == 0 || p.tile != 4096 || m == 0) return nullptr;
+    *dbits = p.bits[0];
+    return carve(ws, m, n).H;
+}
 
 // ------------------------------------------------- row-range partition ---
 // Stable partition of (key, payload) pairs by which of `parts` key ranges
@@ -371,7 +389,7 @@ cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* cou
 
 cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
                               const uint32_t* counts_in, uint32_t* offsets, uint32_t* indices, double* w_out,
-                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s) {
+                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool h1_ready) {
     const bool weighted = w != nullptr;
     CsrWs W = carve(ws, m, n);
     if (ws_bytes < W.total) return cudaErrorInvalidValue;
@@ -397,24 +415,24 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
     }
     const uint32_t* kin = I2;
     const uint32_t* vin = weighted ? nullptr : J2;
+    if (!counts_in) {
+        // offsets come from the last pass's sorted output (row starts + suffix-min)
+        e = cudaMemsetAsync(offsets, 0xFF, (size_t)n * 4, s);
+        if (e == cudaSuccess) e = launch_set_u32(offsets + n, (uint32_t)m, s);
+        if (e != cudaSuccess) return e;
+    }
     for (int i = 0; i < p.passes; i++) {
         const bool last = i == p.passes - 1;
         // pass i writes bufs[2(i&1)], bufs[2(i&1)+1]; it reads the other parity.
-        // The last pass keeps the sorted rows only when offsets come from them.
-        uint32_t* kout = (last && counts_in) ? nullptr : W.bufs[(i & 1) * 2];
+        uint32_t* kout = last ? nullptr : W.bufs[(i & 1) * 2];
         uint32_t* vout = (last && !weighted) ? indices : W.bufs[(i & 1) * 2 + 1];
         e = dispatch_pass(p.v, kin, vin, m, p.shift[i], p.bits[i], W.H, W.scan_status, W.counters, kout, vout,
-                          num_sms, s);
+                          num_sms, s, (last && !counts_in) ? offsets : nullptr, i == 0 && h1_ready);
         if (e != cudaSuccess) return e;
         kin = kout;
         vin = vout;
     }
     if (!counts_in) {
-        // kin = rows in CSR order
-        e = cudaMemsetAsync(offsets, 0xFF, ((size_t)n + 1) * 4, s);
-        if (e != cudaSuccess) return e;
-        const uint64_t blocks = ceil_div(ceil_div(m, 4), 256), cap = (uint64_t)num_sms * 16;
-        k_row_starts<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(kin, m, n, offsets);
         const uint64_t sm_tiles = ceil_div((uint64_t)n + 1, kSmTile);
         unsigned long long* sm_status = W.off_status + ceil_div((uint64_t)n + 1, kOffTile) + 1;
         e = cudaMemsetAsync(sm_status, 0, sm_tiles * 8, s);

@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
                                                               Op op, int bits, uint64_t tiles,
                                                               const uint32_t* __restrict__ H,
                                                               uint32_t* __restrict__ keys_out,
-                                                              uint32_t* __restrict__ vals_out) {
+                                                              uint32_t* __restrict__ vals_out,
+                                                              uint32_t* __restrict__ row_starts) {
     using C = RadixCfg<RB, NT, IPT>;
     constexpr int B = C::B, NW = C::NW, TILE = C::TILE, BPT = C::BPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -280,9 +281,21 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     const int items = rem < (uint64_t)TILE ? (int)rem : TILE;
     for (int j = threadIdx.x; j < items; j += NT) {
         const uint32_t k = s_key[j];
-        const uint32_t g = s_glob[op(k)] + (uint32_t)j;
+        const uint32_t d = op(k);
+        const uint32_t g = s_glob[d] + (uint32_t)j;
         if (keys_out) keys_out[g] = k;
         vals_out[g] = s_val[j];
+        if (row_starts) {
+            // Last (most significant) pass: the output is sorted by key, and this
+            // tile's run for digit d is a contiguous segment of it.  A key change
+            // inside the run is a first occurrence; the run's first item may
+            // continue the previous run, so it only lowers the slot.  Slots start
+            // at 0xFFFFFFFF; empty rows are filled by a suffix-min afterwards.
+            if (j == (int)s_off[d])
+                atomicMin(row_starts + k, g);
+            else if (s_key[j - 1] != k)
+                row_starts[k] = g;
+        }
     }
 }
 

@@ -26,25 +26,29 @@ namespace boba {
 constexpr int kRlNT = 1024;
 constexpr int kHubHistRows = 8192;
 
-template <bool HIST, bool HUBS>
+// MODE: 0 relabel only; 1 + out-degree histogram of the new rows (counts, the
+// np.bincount of graph.py:270); 2 + the first radix pass's per-tile digit
+// histogram (H[d * tiles + t], tile = 4096 edges = one CTA iteration), so
+// COO->CSR can skip that pass's upsweep over I2.
+template <int MODE, bool HUBS>
 __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ I, const uint4* __restrict__ J,
                                                       uint64_t quads, const uint32_t* __restrict__ label,
                                                       const unsigned long long* __restrict__ hubs, HubHash hh,
                                                       uint32_t n, uint4* __restrict__ I2, uint4* __restrict__ J2,
-                                                      uint32_t* counts) {
+                                                      uint32_t* counts, uint32_t* H, uint32_t dmask, uint64_t tiles) {
     extern __shared__ uint32_t sm32[];
     uint32_t* s_tab = sm32;                                                       // kHubWays x kHubBuckets
-    uint32_t* s_hist = sm32 + (HUBS ? kHubWays * kHubBuckets : 0);                // kHubHistRows
+    uint32_t* s_hist = sm32 + (HUBS ? kHubWays * kHubBuckets : 0);                // kHubHistRows or 256
     if (HUBS) {
         const uint4* src = reinterpret_cast<const uint4*>(hubs);
         for (int i = threadIdx.x; i < kHubWays * kHubBuckets / 4; i += kRlNT)
             reinterpret_cast<uint4*>(s_tab)[i] = __ldg(src + i);
     }
-    if (HIST)
+    if (MODE == 1)
         for (int i = threadIdx.x; i < kHubHistRows; i += kRlNT) s_hist[i] = 0;
     __syncthreads();
     const uint32_t tmask = hh.tag_bits ? (1u << hh.tag_bits) - 1u : 0u;
-    // probe the hub table (smem) for every endpoint first; returns 0xFFFFFFFF on a miss
+    // hub table probe (smem); 0xFFFFFFFF on a miss
     auto probe = [&](uint32_t v) -> uint32_t {
         if (HUBS) {
             uint32_t b, tag;
@@ -57,29 +61,51 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ 
         }
         return 0xFFFFFFFFu;
     };
+    auto lookup = [&](uint32_t v) -> uint32_t {
+        const uint32_t h = probe(v);
+        return h != 0xFFFFFFFFu ? h : __ldcg(label + v);
+    };
     auto count = [&](uint32_t r) {
         if (r < (uint32_t)kHubHistRows)
             atomicAdd(s_hist + r, 1u);
         else
             atomicAdd(counts + r, 1u);
     };
-    auto lookup = [&](uint32_t v) -> uint32_t {
-        const uint32_t h = probe(v);
-        return h != 0xFFFFFFFFu ? h : __ldcg(label + v);
-    };
-    const uint64_t stride = (uint64_t)gridDim.x * kRlNT;
-    for (uint64_t q = (uint64_t)blockIdx.x * kRlNT + threadIdx.x; q < quads; q += stride) {
-        const uint4 a = __ldg(I + q), b = __ldg(J + q);
-        uint4 ra, rb;
-        ra.x = lookup(a.x); ra.y = lookup(a.y); ra.z = lookup(a.z); ra.w = lookup(a.w);
-        rb.x = lookup(b.x); rb.y = lookup(b.y); rb.z = lookup(b.z); rb.w = lookup(b.w);
-        I2[q] = ra;
-        J2[q] = rb;
-        if (HIST) {
-            count(ra.x); count(ra.y); count(ra.z); count(ra.w);
+    // One CTA iteration = one 4096-edge tile (kRlNT quads).  MODE 2 double-buffers
+    // the tile histogram so each iteration needs a single barrier: a buffer is
+    // filled in iteration t, flushed (and re-zeroed) right after that barrier,
+    // and refilled only in t + 2, after the next barrier.
+    if (MODE == 2) {
+        for (int i = threadIdx.x; i < 512; i += kRlNT) s_hist[i] = 0;
+        __syncthreads();
+    }
+    int par = 0;
+    for (uint64_t t = blockIdx.x; t * kRlNT < quads; t += gridDim.x, par ^= 1) {
+        uint32_t* hb = s_hist + 256 * par;
+        const uint64_t q = t * kRlNT + threadIdx.x;
+        if (q < quads) {
+            const uint4 a = __ldg(I + q), b = __ldg(J + q);
+            uint4 ra, rb;
+            ra.x = lookup(a.x); ra.y = lookup(a.y); ra.z = lookup(a.z); ra.w = lookup(a.w);
+            rb.x = lookup(b.x); rb.y = lookup(b.y); rb.z = lookup(b.z); rb.w = lookup(b.w);
+            I2[q] = ra;
+            J2[q] = rb;
+            if (MODE == 1) {
+                count(ra.x); count(ra.y); count(ra.z); count(ra.w);
+            } else if (MODE == 2) {
+                atomicAdd(hb + (ra.x & dmask), 1u); atomicAdd(hb + (ra.y & dmask), 1u);
+                atomicAdd(hb + (ra.z & dmask), 1u); atomicAdd(hb + (ra.w & dmask), 1u);
+            }
+        }
+        if (MODE == 2) {
+            __syncthreads();
+            for (int i = threadIdx.x; i <= (int)dmask; i += kRlNT) {
+                H[(uint64_t)i * tiles + t] = hb[i];
+                hb[i] = 0;
+            }
         }
     }
-    if (HIST) {
+    if (MODE == 1) {
         __syncthreads();
         for (int i = threadIdx.x; i < kHubHistRows && i < (int)n; i += kRlNT)
             if (s_hist[i]) atomicAdd(counts + i, s_hist[i]);
@@ -99,22 +125,23 @@ __global__ void k_relabel_scalar(const uint32_t* __restrict__ I, const uint32_t*
     }
 }
 
-template <bool HIST, bool HUBS>
+template <int MODE, bool HUBS>
 static void launch_vec(int grid, size_t smem, cudaStream_t s, const uint32_t* I, const uint32_t* J, uint64_t quads,
                        const uint32_t* label, const unsigned long long* hubs, uint32_t n, uint32_t* I2, uint32_t* J2,
-                       uint32_t* counts) {
+                       uint32_t* counts, uint32_t* H, uint32_t dmask, uint64_t tiles) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_relabel<HIST, HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_relabel<MODE, HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_relabel<HIST, HUBS><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs,
-                                                    HubHash::make(n), n, (uint4*)I2, (uint4*)J2, counts);
+    k_relabel<MODE, HUBS><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs,
+                                                    HubHash::make(n), n, (uint4*)I2, (uint4*)J2, counts, H, dmask,
+                                                    tiles);
 }
 
 cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,
                            const unsigned long long* hubs, uint32_t* I2, uint32_t* J2, uint32_t* counts, uint32_t n,
-                           int num_sms, cudaStream_t s) {
+                           int num_sms, cudaStream_t s, uint32_t* H, int dbits) {
     if (counts) {
         cudaError_t err = cudaMemsetAsync(counts, 0, (size_t)n * 4, s);
         if (err != cudaSuccess) return err;
@@ -122,6 +149,7 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
     if (m == 0) return cudaSuccess;
     const bool vec = ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(J) |
                        reinterpret_cast<uintptr_t>(I2) | reinterpret_cast<uintptr_t>(J2)) & 15) == 0;
+    if (H && (!vec || (m & 3) || counts)) return cudaErrorInvalidValue;  // caller falls back to the upsweep
     uint64_t done = 0;
     if (vec && m >= 4) {
         const uint64_t quads = m >> 2;
@@ -133,15 +161,19 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
         // vertices the gathers are DRAM-latency bound and the probe only delays them
         // (c5, n = 2^24: 2.26 ms without, 3.28 ms with).
         if (n > (1u << 23) || getenv("BOBA_NO_HUBS")) hubs = nullptr;
-        const size_t smem = (hubs ? kHubTableBytes : 0) + 4 * (counts ? kHubHistRows : 0);
-        if (counts && hubs)
-            launch_vec<true, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
-        else if (counts)
-            launch_vec<true, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
-        else if (hubs)
-            launch_vec<false, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
-        else
-            launch_vec<false, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
+        const uint32_t dmask = H ? (1u << dbits) - 1u : 0u;
+        const uint64_t tiles = ceil_div(m, 4 * kRlNT);
+        const size_t smem = (hubs ? kHubTableBytes : 0) + 4 * (counts ? kHubHistRows : (H ? 512 : 0));
+        if (counts) {
+            if (hubs) launch_vec<1, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
+            else launch_vec<1, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
+        } else if (H) {
+            if (hubs) launch_vec<2, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
+            else launch_vec<2, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
+        } else {
+            if (hubs) launch_vec<0, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
+            else launch_vec<0, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
+        }
         done = quads * 4;
     }
     if (done < m) {
