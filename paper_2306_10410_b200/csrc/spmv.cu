@@ -74,53 +74,58 @@ __global__ void k_spmv_partition(const uint32_t* __restrict__ offsets, uint32_t 
     coords[b] = (uint32_t)merge_search(offsets + 1, n, 0, m, d);
 }
 
-// Main pass: every row that ends inside a CTA is written here; the first row
-// a CTA ends may have started in earlier CTAs -- its partial sum is written
-// and fixed up by k_spmv_carry (no CTA ever waits on another).
+__device__ __forceinline__ void group_bar(int id) {
+    if (id == 0)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kSpNT) : "memory");
+}
+
+// One merge-path tile processed by kSpNT threads (gt = thread index within
+// the group, bar = the group's barrier id).  Every row that ends inside the
+// tile is written here; the first row the tile ends may have started in
+// earlier tiles -- its partial sum is written and fixed up by k_spmv_carry (no
+// tile ever waits on another).  x entries below kx come from shared memory.
 template <typename T>
-__global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict__ offsets,
-                                                      const uint32_t* __restrict__ indices,
-                                                      const T* __restrict__ w, const T* __restrict__ x,
-                                                      T* __restrict__ y, uint32_t n, uint64_t m,
-                                                      const uint32_t* __restrict__ coords,
-                                                      uint32_t* __restrict__ tile_head, T* __restrict__ tile_tail) {
+__device__ __forceinline__ void spmv_tile(uint64_t tile, int gt, int bar, const uint32_t* __restrict__ offsets,
+                                          const uint32_t* __restrict__ indices, const T* __restrict__ w,
+                                          const T* __restrict__ x, T* __restrict__ y, uint32_t n, uint64_t m,
+                                          const uint32_t* __restrict__ coords, uint32_t* __restrict__ tile_head,
+                                          T* __restrict__ tile_tail, uint32_t* s_end, T* s_val, SegValT<T>* s_warp,
+                                          const T* s_x, uint32_t kx) {
     using SegVal = SegValT<T>;
-    __shared__ uint32_t s_end[kSpTile + 1];
-    __shared__ T s_val[kSpTile];
-    __shared__ SegVal s_warp[kSpNT / 32];
-    const uint64_t tile = blockIdx.x;
     const uint64_t total = (uint64_t)n + m;
     const uint64_t d0 = tile * kSpTile;
     const uint64_t d1 = d0 + kSpTile < total ? d0 + kSpTile : total;
     const uint64_t i0 = __ldg(coords + tile), i1 = __ldg(coords + tile + 1);
     const uint64_t j0 = d0 - i0, j1 = d1 - i1;
     const uint32_t nrows = (uint32_t)(i1 - i0), nnz = (uint32_t)(j1 - j0);
-    for (uint32_t k = threadIdx.x; k <= nrows; k += kSpNT)
+    for (uint32_t k = gt; k <= nrows; k += kSpNT)
         s_end[k] = (i0 + k < n) ? ld_stream_u32(offsets + i0 + 1 + k) : 0xFFFFFFFFu;
     {
         // all index loads, then all x gathers in flight together (nnz <= kSpTile)
         uint32_t col[kSpIPT];
 #pragma unroll
         for (int u = 0; u < kSpIPT; u++) {
-            const uint32_t k = threadIdx.x + u * kSpNT;
+            const uint32_t k = gt + u * kSpNT;
             col[u] = k < nnz ? ld_stream_u32(indices + j0 + k) : 0u;
         }
         T p[kSpIPT];
 #pragma unroll
         for (int u = 0; u < kSpIPT; u++) {
-            const uint32_t k = threadIdx.x + u * kSpNT;
-            p[u] = k < nnz ? __ldg(x + col[u]) : T(0);
+            const uint32_t k = gt + u * kSpNT;
+            p[u] = k < nnz ? (col[u] < kx ? s_x[col[u]] : __ldg(x + col[u])) : T(0);
         }
 #pragma unroll
         for (int u = 0; u < kSpIPT; u++) {
-            const uint32_t k = threadIdx.x + u * kSpNT;
+            const uint32_t k = gt + u * kSpNT;
             if (k < nnz) s_val[k] = w ? p[u] * __ldg(w + j0 + k) : p[u];
         }
     }
-    __syncthreads();
+    group_bar(bar);
     // Per-thread sequential fold over kSpIPT merge items.
     const uint32_t items_tile = (uint32_t)(d1 - d0);
-    const uint32_t diag = threadIdx.x * kSpIPT < items_tile ? threadIdx.x * kSpIPT : items_tile;
+    const uint32_t diag = gt * kSpIPT < items_tile ? gt * kSpIPT : items_tile;
     uint32_t it = (uint32_t)merge_search(s_end, nrows, j0, nnz, diag);
     uint32_t jt = diag - it;
     const uint32_t items = items_tile - diag < (uint32_t)kSpIPT ? items_tile - diag : (uint32_t)kSpIPT;
@@ -144,8 +149,8 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
             it++;
         }
     }
-    // CTA segmented scan of (emitted, tail) -> exclusive carry per thread.
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    // Segmented scan of (emitted, tail) over the group -> exclusive carry per thread.
+    const unsigned lane = lane_id(), warp = gt >> 5;
     SegVal inc{emitted, acc};
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
     lex.v = __shfl_up_sync(0xFFFFFFFFu, inc.v, 1);
     if (lane == 0) lex = SegVal{false, T(0)};
     if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
+    group_bar(bar);
     if (warp == 0) {
         SegVal wi = lane < kSpNT / 32 ? s_warp[lane] : SegVal{false, T(0)};
 #pragma unroll
@@ -176,16 +181,31 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
         __syncwarp();
         if (lane < kSpNT / 32) s_warp[lane] = we;
         if (lane == kSpNT / 32 - 1) {
-            tile_tail[tile] = wi.v;                    // CTA aggregate (flag = has a head row)
+            tile_tail[tile] = wi.v;                    // tile aggregate (flag = has a head row)
             if (!wi.f) tile_head[tile] = 0xFFFFFFFFu;  // no row ends here
         }
     }
-    __syncthreads();
+    group_bar(bar);
     if (emitted) {
         const SegVal ex = seg_combine(s_warp[warp], lex);
         y[first_row] = first_val + ex.v;
-        if (!ex.f) tile_head[tile] = (uint32_t)first_row;  // partial: earlier CTAs add their tails
+        if (!ex.f) tile_head[tile] = (uint32_t)first_row;  // partial: earlier tiles add their tails
     }
+}
+
+// One tile per CTA (small problems, no x cache).
+template <typename T>
+__global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict__ offsets,
+                                                      const uint32_t* __restrict__ indices,
+                                                      const T* __restrict__ w, const T* __restrict__ x,
+                                                      T* __restrict__ y, uint32_t n, uint64_t m,
+                                                      const uint32_t* __restrict__ coords,
+                                                      uint32_t* __restrict__ tile_head, T* __restrict__ tile_tail) {
+    __shared__ uint32_t s_end[kSpTile + 1];
+    __shared__ T s_val[kSpTile];
+    __shared__ SegValT<T> s_warp[kSpNT / 32];
+    spmv_tile<T>(blockIdx.x, threadIdx.x, 0, offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail, s_end,
+                 s_val, s_warp, nullptr, 0u);
 }
 
 // Chunk aggregates of the per-CTA (has_head, tail) pairs: a segmented sum
@@ -303,14 +323,11 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
     T* tile_tail = reinterpret_cast<T*>(p + 2 * arr);
     unsigned* chunk_flag = reinterpret_cast<unsigned*>(p + 3 * arr);
     T* chunk_val = reinterpret_cast<T*>(p + 3 * arr + ((chunks + 1) * 4 + 15) / 16 * 16);
-    static int carve = -2;
-    if (carve == -2) {
-        const char* e = getenv("BOBA_SPMV_CARVEOUT");
-        carve = e ? atoi(e) : -1;
-        if (carve >= 0) cudaFuncSetAttribute(k_spmv_merge<T>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-    }
     k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
-    k_spmv_merge<T><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail);
+    // (A persistent variant with a 128 KB shared-memory copy of the hub prefix of x
+    // was measured slower at c2/c3: the occupancy it costs outweighs the hits.)
+    k_spmv_merge<T><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head,
+                                                      tile_tail);
     if (tiles > 1) {
         k_spmv_chunk_agg<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val);
         k_spmv_carry<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val, y);
