@@ -60,6 +60,18 @@ def alg_bytes(m, n):
     }
 
 
+def measured_traffic(cfg):
+    """DRAM bytes per phase from the committed ncu --set full capture
+    (profiles/traffic.json; measured on c2 only)."""
+    if cfg != "c2":
+        return {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)["phases"]
+    except Exception:
+        return {}
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -283,17 +295,19 @@ def run_ours(args):
     # ---- roofline per phase
     hbm, peak_kind = peaks()
     ab = alg_bytes(m, n)
+    traffic = measured_traffic(cfg)
     phases = {}
     for k in phase_names:
         t = statistics.mean(phase_ms[k]) / 1e3
         ach = ab[k] / t / 1e9
         phases[k] = {"ms": round(t * 1e3, 4), "alg_bytes": int(ab[k]), "gbs": round(ach, 1),
-                     "frac": round(ach / hbm, 4)}
+                     "frac": round(ach / hbm, 4), "dram_bytes_ncu": traffic.get(k)}
     dom = max(phase_names, key=lambda k: phases[k]["ms"])
     total_alg = sum(ab.values())
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": phases[dom]["gbs"], "peak": hbm, "peak_kind": peak_kind,
-        "unit": "GB/s", "frac": phases[dom]["frac"], "traffic": None,
+        "unit": "GB/s", "frac": phases[dom]["frac"], "traffic": traffic.get(dom),
+        "traffic_source": "profiles/traffic.json (ncu --set full, DRAM read+write per launch)" if traffic else None,
         "pipeline_frac": round(total_alg / (ms_step / 1e3) / 1e9 / hbm, 4),
         "pipeline_alg_bytes": int(total_alg), "phases": phases,
     }
