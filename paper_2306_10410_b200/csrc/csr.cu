@@ -194,6 +194,7 @@ Variant variant() {
     const char* e = getenv("BOBA_RADIX_CFG");
     if (e && e[0] == '1') return Variant::R11x256;
     if (e && e[0] == 'b') return Variant::R8x512;
+
     return Variant::R8x256;
 }
 int variant_bits(Variant v) { return v == Variant::R11x256 ? 11 : 8; }
@@ -201,6 +202,7 @@ uint64_t variant_tile(Variant v) {
     switch (v) {
         case Variant::R8x256: return RadixCfg<8, 256, 16>::TILE;
         case Variant::R8x512: return RadixCfg<8, 512, 16>::TILE;
+
         default: return RadixCfg<11, 256, 16>::TILE;
     }
 }
@@ -308,6 +310,7 @@ cudaError_t dispatch_pass(Variant v, const uint32_t* kin, const uint32_t* vin, u
         case Variant::R8x512:
             return radix_pass<8, 512, 16, 2>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s, row_starts,
                                              skip_up);
+
         default:
             return radix_pass<11, 256, 16, 2>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s,
                                               row_starts, skip_up);

@@ -50,7 +50,7 @@ struct RadixCfg {
     static constexpr int RAW_BYTES = TILE * 4;                      // payloads prefetched by cp.async
     static constexpr size_t SMEM = (size_t)HIST_BYTES + STAGE_BYTES + RAW_BYTES + 2 * B * 4;  // + s_off, s_glob
     static_assert(TILE < 65536, "16-bit counters and packed ranks");
-    static_assert(B % NT == 0 || NT % B == 0, "digit ownership");
+    static_assert(B % NT == 0 || NT >= B, "digit ownership");
 };
 
 // ------------------------------------------------------------- upsweep ---
