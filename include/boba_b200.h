@@ -186,6 +186,43 @@ int boba_range_partition(const uint32_t *keys, const uint32_t *vals, uint64_t m,
 /* out[i] = src[idx[i]] (permutation application on vertex arrays). */
 int boba_gather_u32(const uint32_t *src, const uint32_t *idx, uint64_t count, uint32_t *out,
                     void *stream);
+/* --- Orderings and edge sorts beside BOBA ----------------
+ * deg[v] = #{e : I[e] == v} + #{e : J[e] == v}: total degree, reference
+ * graph.degrees (graph.py:297-300). */
+int boba_total_degrees(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n, uint32_t *deg,
+                       void *stream);
+/* Degree ordering: order = vertices by descending total degree, ties by
+ * ascending id (np.lexsort((arange(n), -deg))); label[order[k]] = k.
+ * Replaces ordering.degree_order (ordering.py:160-164). */
+size_t boba_degree_order_workspace_size(uint64_t m, uint32_t n);
+int boba_degree_order(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n, uint32_t *order,
+                      uint32_t *label, void *workspace, size_t workspace_bytes, void *stream);
+/* Hub ordering: vertices with total degree above the mean (deg * n > 2m)
+ * first by descending degree, ties by id; the rest after them in id order.
+ * Workspace as boba_degree_order.  Replaces ordering.hub_order
+ * (ordering.py:167-176). */
+int boba_hub_order(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n, uint32_t *order,
+                   uint32_t *label, void *workspace, size_t workspace_bytes, void *stream);
+/* Stable sort of the edge list by destination J (ties keep edge order),
+ * weights (float64, may be NULL) move bit-exactly.  Replaces
+ * graph.sort_coo_by_destination (graph.py:303-307). */
+size_t boba_sort_coo_by_destination_workspace_size(uint64_t m, uint32_t n);
+int boba_sort_coo_by_destination(const uint32_t *I, const uint32_t *J, const double *w, uint64_t m,
+                                 uint32_t n, uint32_t *I_out, uint32_t *J_out, double *w_out,
+                                 void *workspace, size_t workspace_bytes, void *stream);
+
+/* PageRank by power iteration on a forward CSR (row v = out-neighbours):
+ * uniform teleport, dangling mass redistributed uniformly, stop when the L1
+ * change < tol or after max_iters rounds; x (n float64) receives the ranks,
+ * *iterations (device uint32, may be NULL) the rounds run.  Fully
+ * device-resident (no host synchronisation per round), deterministic.
+ * Replaces kernels.pagerank (kernels.py:57-107); BOBA_EINVAL unless
+ * 0 < damping < 1 (the reference's ValueError). */
+size_t boba_pagerank_workspace_size(uint32_t n, uint64_t m);
+int boba_pagerank(const uint32_t *offsets, const uint32_t *indices, const double *w, uint32_t n,
+                  uint64_t m, double damping, double tol, int max_iters, double *x,
+                  uint32_t *iterations, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Graph500 R-MAT (a,b,c,d = .57,.19,.19,.05), m = edge_factor << scale
  * i.i.d. edges in generation order; identical to oracle_rmat_edges. */
 int boba_generate_rmat(int scale, uint64_t m, uint64_t seed, uint32_t *I, uint32_t *J, void *stream);

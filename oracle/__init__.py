@@ -56,6 +56,9 @@ def _load():
         "oracle_label_from_order": ([_P, _I64, _P], None),
         "oracle_apply_permutation": ([_P, _P, _I64, _P, _P, _P], None),
         "oracle_degrees": ([_P, _I64, _I64, _P], None),
+        "oracle_total_degrees": ([_P, _P, _I64, _I64, _P], None),
+        "oracle_degree_order": ([_P, _P, _I64, _I64, ctypes.c_int, _P], None),
+        "oracle_sort_by_destination": ([_P, _P, _P, _I64, _I64, _P, _P, _P], None),
         "oracle_coo_to_csr": ([_P, _P, _P, _I64, _I64, _P, _P, _P], None),
         "oracle_spmv_pull": ([_P, _P, _P, _P, _I64, _P], None),
         "oracle_rmat_edges": ([ctypes.c_int, _I64, ctypes.c_uint64, _I64, _I64, _P, _P], None),
@@ -136,6 +139,32 @@ def degrees(I, n):
     return d
 
 
+def total_degrees(I, J, n):
+    """reference graph.py:297-300."""
+    I, J = _i64(I), _i64(J)
+    d = np.empty(n, np.int64)
+    _load().oracle_total_degrees(_ptr(I), _ptr(J), I.size, n, _ptr(d))
+    return d
+
+
+def degree_order(I, J, n, hub=False):
+    """reference ordering.py:160-164 (degree_order) / 167-176 (hub_order) -> order."""
+    I, J = _i64(I), _i64(J)
+    order = np.empty(n, np.int64)
+    _load().oracle_degree_order(_ptr(I), _ptr(J), I.size, n, int(bool(hub)), _ptr(order))
+    return order
+
+
+def sort_coo_by_destination(I, J, n, weights=None):
+    """reference graph.py:303-307 -> (I, J, weights)."""
+    I, J = _i64(I), _i64(J)
+    W = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    I2, J2 = np.empty_like(I), np.empty_like(J)
+    W2 = None if W is None else np.empty(I.size, np.float64)
+    _load().oracle_sort_by_destination(_ptr(I), _ptr(J), _ptr(W), I.size, n, _ptr(I2), _ptr(J2), _ptr(W2))
+    return I2, J2, W2
+
+
 def coo_to_csr(I, J, n, weights=None):
     """reference graph.py:253-277 + _parallel.py:55-88 -> (offsets, indices, weights)."""
     I, J = _i64(I), _i64(J)
@@ -156,6 +185,34 @@ def spmv_pull(offsets, indices, x, weights=None):
     y = np.empty(n, np.float64)
     _load().oracle_spmv_pull(_ptr(offsets), _ptr(indices), _ptr(W), _ptr(x), n, _ptr(y))
     return y
+
+
+def pagerank(offsets, indices, x0_n, weights=None, damping=0.85, tol=1e-6, max_iters=100):
+    """reference kernels.py:57-107, restated with the oracle's own CSR and
+    SpMV (sequential row sums) -> (x, iterations)."""
+    offsets, indices = _i64(offsets), _i64(indices)
+    n = int(x0_n)
+    if n == 0:
+        return np.zeros(0), 0
+    m = indices.size
+    fw = np.ones(m) if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    deg = np.diff(offsets)
+    src = np.repeat(np.arange(n, dtype=np.int64), deg)
+    ow = spmv_pull(offsets, indices, np.ones(n), fw)   # row sums of the forward weights (kernels.py:88)
+    dangling = ow == 0.0
+    share = fw / np.repeat(np.where(dangling, 1.0, ow), deg)
+    roff, ridx, rw = coo_to_csr(indices, src, n, share)
+    x = np.full(n, 1.0 / n)
+    tele = (1.0 - damping) / n
+    it = 0
+    for it in range(1, max_iters + 1):
+        dm = x[dangling].sum() / n
+        xn = damping * (spmv_pull(roff, ridx, x, rw) + dm) + tele
+        delta = np.abs(xn - x).sum()
+        x = xn
+        if delta < tol:
+            break
+    return x, it
 
 
 def rmat_edges(scale, edge_factor, seed, e0=0, e1=None):

@@ -10,17 +10,22 @@ same phases on device-resident CUDA tensors.
 """
 
 from .errors import BobaError, MalformedGraphError, ParseError, UndefinedMetricError
-from .graph import CooGraph, CsrGraph, Permutation, apply_permutation, coo_to_csr, degrees
-from .kernels import spmv_pull
+from .graph import (CooGraph, CsrGraph, Permutation, apply_permutation, coo_to_csr, degrees, sort_coo_by_destination,
+                    total_degrees)
+from .kernels import pagerank, spmv_pull
 from .ordering import (
     ORDERING_CHOICES,
     RANK_UNSET,
     BobaOrder,
+    DegreeOrder,
+    HubOrder,
     IdentityOrder,
     RandomOrder,
     boba_parallel,
     boba_sequential,
     compute_ordering,
+    degree_order,
+    hub_order,
     identity_order,
     random_order,
 )
@@ -31,7 +36,8 @@ __version__ = "0.1.0"
 __all__ = [
     "BobaError", "MalformedGraphError", "ParseError", "UndefinedMetricError",
     "CooGraph", "CsrGraph", "Permutation", "apply_permutation", "coo_to_csr", "degrees",
-    "spmv_pull", "RANK_UNSET", "ORDERING_CHOICES", "boba_parallel", "boba_sequential",
-    "compute_ordering", "random_order", "identity_order", "BobaOrder", "RandomOrder", "IdentityOrder",
+    "total_degrees", "sort_coo_by_destination", "spmv_pull", "pagerank", "RANK_UNSET", "ORDERING_CHOICES", "boba_parallel", "boba_sequential",
+    "compute_ordering", "random_order", "identity_order", "degree_order", "hub_order", "BobaOrder", "RandomOrder",
+    "IdentityOrder", "DegreeOrder", "HubOrder",
     "__version__",
 ]

@@ -82,6 +82,33 @@ def degrees(I, n: int) -> np.ndarray:
     return to_host_ids(D.degrees(dI, n))
 
 
+def total_degrees(I, J, n: int) -> np.ndarray:
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    return to_host_ids(D.total_degrees(to_device_ids(I, n, "I"), to_device_ids(J, n, "J"), n))
+
+
+def degree_order(I, J, n: int, hub: bool = False):
+    """-> (order, label) int64."""
+    if n == 0:
+        e = np.empty(0, dtype=np.int64)
+        return e, e.copy()
+    order, label = D.degree_order(to_device_ids(I, n, "I"), to_device_ids(J, n, "J"), n, hub=hub)
+    return to_host_ids(order), to_host_ids(label)
+
+
+def sort_coo_by_destination(I, J, n: int, weights=None):
+    m = int(np.asarray(I).size)
+    if m == 0:
+        e = np.empty(0, dtype=np.int64)
+        return e, e.copy(), (None if weights is None else np.empty(0, dtype=np.float64))
+    w = None
+    if weights is not None:
+        w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(_dev())
+    Io, Jo, wo = D.sort_coo_by_destination(to_device_ids(I, n, "I"), to_device_ids(J, n, "J"), n, w)
+    return to_host_ids(Io), to_host_ids(Jo), (None if wo is None else wo.cpu().numpy())
+
+
 def coo_to_csr(I, J, n: int, weights=None):
     dI, dJ = to_device_ids(I, n, "I"), to_device_ids(J, n, "J")
     w = None
@@ -101,3 +128,13 @@ def spmv(offsets, indices, x, weights=None) -> np.ndarray:
     dx = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
     dw = None if weights is None else torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
     return D.spmv(do, di, dx, dw).cpu().numpy()
+
+
+def pagerank(offsets, indices, n: int, weights, damping: float, tol: float, max_iters: int):
+    m = int(np.asarray(indices).size)
+    dev = _dev()
+    do = to_device_ids(offsets, m + 1, "offsets")
+    di = to_device_ids(indices, max(n, 1), "indices") if m else torch.empty(0, dtype=D.ID, device=dev)
+    dw = None if weights is None else torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
+    x, it = D.pagerank(do, di, dw, damping, tol, max_iters)
+    return x.cpu().numpy(), int(it.cpu()[0])

@@ -30,6 +30,7 @@ _P = ctypes.c_void_p
 _U64 = ctypes.c_uint64
 _U32 = ctypes.c_uint32
 _I = ctypes.c_int
+_D = ctypes.c_double
 _SZ = ctypes.c_size_t
 
 # name -> (argtypes, restype); mirrors include/boba_b200.h one to one.
@@ -65,6 +66,14 @@ SIGNATURES = {
     "boba_range_partition_workspace_size": ([_U64, _I], _SZ),
     "boba_range_partition": ([_P, _P, _U64, _P, _I, _P, _P, _P, _P, _SZ, _P], _I),
     "boba_gather_u32": ([_P, _P, _U64, _P, _P], _I),
+    "boba_total_degrees": ([_P, _P, _U64, _U32, _P, _P], _I),
+    "boba_degree_order_workspace_size": ([_U64, _U32], _SZ),
+    "boba_degree_order": ([_P, _P, _U64, _U32, _P, _P, _P, _SZ, _P], _I),
+    "boba_hub_order": ([_P, _P, _U64, _U32, _P, _P, _P, _SZ, _P], _I),
+    "boba_sort_coo_by_destination_workspace_size": ([_U64, _U32], _SZ),
+    "boba_sort_coo_by_destination": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _SZ, _P], _I),
+    "boba_pagerank_workspace_size": ([_U32, _U64], _SZ),
+    "boba_pagerank": ([_P, _P, _P, _U32, _U64, _D, _D, _I, _P, _P, _P, _SZ, _P], _I),
     "boba_generate_rmat": ([_I, _U64, _U64, _P, _P, _P], _I),
     "boba_generate_rmat_range": ([_I, _U64, _U64, _U64, _P, _P, _P], _I),
     "boba_generate_grid": ([_U32, _U32, _P, _P, _P], _I),

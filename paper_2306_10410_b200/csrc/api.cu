@@ -368,6 +368,72 @@ int boba_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, ui
     return cuda_status(boba::launch_gather_u32(src, idx, count, out, num_sms(), S(stream)), "boba_gather_u32");
 }
 
+int boba_total_degrees(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* deg, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_total_degrees")) return rc;
+    if (n == 0) return BOBA_OK;
+    REQUIRE(deg && ((I && J) || m == 0), "boba_total_degrees: NULL argument");
+    return cuda_status(boba::launch_total_degrees(I, J, m, n, deg, num_sms(), S(stream)), "boba_total_degrees");
+}
+
+size_t boba_degree_order_workspace_size(uint64_t m, uint32_t n) { return boba::degree_order_workspace_bytes(m, n); }
+
+int boba_degree_order(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* order, uint32_t* label,
+                      void* ws, size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_degree_order")) return rc;
+    if (n == 0) return BOBA_OK;
+    REQUIRE(order && label && ws && ((I && J) || m == 0), "boba_degree_order: NULL argument");
+    REQUIRE(ws_bytes >= boba::degree_order_workspace_bytes(m, n), "boba_degree_order: workspace too small");
+    return cuda_status(boba::launch_degree_order(I, J, m, n, order, label, ws, ws_bytes, num_sms(), S(stream), false),
+                       "boba_degree_order");
+}
+
+int boba_hub_order(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* order, uint32_t* label,
+                   void* ws, size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_hub_order")) return rc;
+    if (n == 0) return BOBA_OK;
+    REQUIRE(order && label && ws && ((I && J) || m == 0), "boba_hub_order: NULL argument");
+    REQUIRE(ws_bytes >= boba::degree_order_workspace_bytes(m, n), "boba_hub_order: workspace too small");
+    return cuda_status(boba::launch_degree_order(I, J, m, n, order, label, ws, ws_bytes, num_sms(), S(stream), true),
+                       "boba_hub_order");
+}
+
+size_t boba_sort_coo_by_destination_workspace_size(uint64_t m, uint32_t n) {
+    return boba::sort_by_destination_workspace_bytes(m, n);
+}
+
+int boba_sort_coo_by_destination(const uint32_t* I, const uint32_t* J, const double* w, uint64_t m, uint32_t n,
+                                 uint32_t* I_out, uint32_t* J_out, double* w_out, void* ws, size_t ws_bytes,
+                                 void* stream) {
+    if (int rc = check_sizes(m, n, "boba_sort_coo_by_destination")) return rc;
+    if (m == 0) return BOBA_OK;
+    REQUIRE(I && J && I_out && J_out && ws, "boba_sort_coo_by_destination: NULL argument");
+    REQUIRE(!w || w_out, "boba_sort_coo_by_destination: weights given but weights_out is NULL");
+    REQUIRE(ws_bytes >= boba::sort_by_destination_workspace_bytes(m, n),
+            "boba_sort_coo_by_destination: workspace too small");
+    return cuda_status(boba::launch_sort_by_destination(I, J, w, m, n, I_out, J_out, w_out, ws, ws_bytes, num_sms(),
+                                                        S(stream)),
+                       "boba_sort_coo_by_destination");
+}
+
+size_t boba_pagerank_workspace_size(uint32_t n, uint64_t m) {
+    return boba::pagerank_workspace_bytes(n, m, num_sms());
+}
+
+int boba_pagerank(const uint32_t* offsets, const uint32_t* indices, const double* w, uint32_t n, uint64_t m,
+                  double damping, double tol, int max_iters, double* x, uint32_t* iterations, void* ws,
+                  size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_pagerank")) return rc;
+    REQUIRE(damping > 0.0 && damping < 1.0, "damping must lie strictly between 0 and 1, got %g", damping);
+    REQUIRE(max_iters >= 0, "boba_pagerank: max_iters must be non-negative");
+    if (n == 0) return cuda_status(iterations ? cudaMemsetAsync(iterations, 0, 4, S(stream)) : cudaSuccess,
+                                   "boba_pagerank");
+    REQUIRE(offsets && x && ws && (indices || m == 0), "boba_pagerank: NULL argument");
+    REQUIRE(ws_bytes >= boba::pagerank_workspace_bytes(n, m, num_sms()), "boba_pagerank: workspace too small");
+    return cuda_status(boba::launch_pagerank(offsets, indices, w, n, m, damping, tol, max_iters, x, iterations, ws,
+                                             ws_bytes, num_sms(), S(stream)),
+                       "boba_pagerank");
+}
+
 int boba_generate_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32_t* J, void* stream) {
     REQUIRE(scale >= 0 && scale <= 32, "boba_generate_rmat: scale out of range");
     REQUIRE((I && J) || m == 0, "boba_generate_rmat: NULL argument");

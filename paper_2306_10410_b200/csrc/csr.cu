@@ -327,6 +327,83 @@ uint32_t* csr_first_pass_hist(void* ws, uint64_t m, uint32_t n, int* dbits) {
     return carve(ws, m, n).H;
 }
 
+__global__ void k_iota(uint32_t* out, uint64_t count) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) out[i] = (uint32_t)i;
+}
+
+cudaError_t launch_iota(uint32_t* out, uint64_t count, int num_sms, cudaStream_t s) {
+    const uint64_t blocks = ceil_div(count, 256), cap = (uint64_t)num_sms * 8;
+    k_iota<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(out, count);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------ generic stable sort ---
+// Stable LSD sort of (key, payload) pairs on the low key_bits of the key, 8-bit
+// digits (the radix passes of COO->CSR).  vals == NULL: payload = input index.
+// Used by the degree ordering (key = ~degree) and by sort_coo_by_destination.
+namespace {
+struct SortWs {
+    uint32_t* bufs[4];
+    uint32_t* H;
+    unsigned long long* st;
+    unsigned* counter;
+    size_t total;
+};
+SortWs carve_sort(void* base, uint64_t count, int key_bits) {
+    SortWs w{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) & ~size_t(255);
+        return base ? static_cast<char*>(base) + o : nullptr;
+    };
+    for (int i = 0; i < 4; i++) w.bufs[i] = (uint32_t*)take(count * 4 + 16);
+    const uint64_t tiles = ceil_div(count ? count : 1, RadixCfg<8, 256, 16>::TILE);
+    const uint64_t hcount = tiles * 256;
+    w.H = (uint32_t*)take(hcount * 4 + 16);
+    w.st = (unsigned long long*)take((ceil_div(hcount, kScanTile) + 1) * 8);
+    w.counter = (unsigned*)take(64);
+    w.total = off;
+    (void)key_bits;
+    return w;
+}
+}  // namespace
+
+size_t sort_pairs_workspace_bytes(uint64_t count, int key_bits) { return carve_sort(nullptr, count, key_bits).total; }
+
+cudaError_t launch_sort_pairs(const uint32_t* keys, const uint32_t* vals, uint64_t count, int key_bits,
+                              uint32_t* keys_out, uint32_t* vals_out, void* ws, size_t ws_bytes, int num_sms,
+                              cudaStream_t s) {
+    SortWs W = carve_sort(ws, count, key_bits);
+    if (ws_bytes < W.total || key_bits < 0 || key_bits > 32) return cudaErrorInvalidValue;
+    if (count == 0) return cudaSuccess;
+    const int passes = (key_bits + 7) / 8;
+    if (passes == 0) {
+        cudaError_t e = cudaSuccess;
+        if (keys_out) e = cudaMemcpyAsync(keys_out, keys, count * 4, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return e;
+        if (vals) return cudaMemcpyAsync(vals_out, vals, count * 4, cudaMemcpyDeviceToDevice, s);
+        return launch_iota(vals_out, count, num_sms, s);
+    }
+    const uint32_t* kin = keys;
+    const uint32_t* vin = vals;
+    int sh = 0;
+    for (int i = 0; i < passes; i++) {
+        const int bits = key_bits / passes + (i < key_bits % passes ? 1 : 0);
+        const bool last = i == passes - 1;
+        uint32_t* kout = last ? keys_out : W.bufs[(i & 1) * 2];
+        uint32_t* vout = last ? vals_out : W.bufs[(i & 1) * 2 + 1];
+        cudaError_t e = radix_pass<8, 256, 16, 4>(kin, vin, count, sh, bits, W.H, W.st, W.counter, kout, vout,
+                                                  num_sms, s, nullptr, false);
+        if (e != cudaSuccess) return e;
+        kin = kout;
+        vin = vout;
+        sh += bits;
+    }
+    return cudaSuccess;
+}
+
 // ------------------------------------------------- row-range partition ---
 // Stable partition of (key, payload) pairs by which of `parts` key ranges
 // [bounds[p], bounds[p+1]) the key falls in -- the send side of the

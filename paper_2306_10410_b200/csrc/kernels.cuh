@@ -61,6 +61,27 @@ size_t range_partition_workspace_bytes(uint64_t m, int parts);
 cudaError_t launch_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds,
                                    int parts, uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out, void* ws,
                                    size_t ws_bytes, int num_sms, cudaStream_t s);
+cudaError_t launch_iota(uint32_t* out, uint64_t count, int num_sms, cudaStream_t s);
+size_t sort_pairs_workspace_bytes(uint64_t count, int key_bits);
+cudaError_t launch_sort_pairs(const uint32_t* keys, const uint32_t* vals, uint64_t count, int key_bits,
+                              uint32_t* keys_out, uint32_t* vals_out, void* ws, size_t ws_bytes, int num_sms,
+                              cudaStream_t s);
+size_t degree_order_workspace_bytes(uint64_t m, uint32_t n);
+cudaError_t launch_total_degrees(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* deg,
+                                 int num_sms, cudaStream_t s);
+cudaError_t launch_degree_order(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* order,
+                                uint32_t* label, void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool hub);
+size_t sort_by_destination_workspace_bytes(uint64_t m, uint32_t n);
+cudaError_t launch_sort_by_destination(const uint32_t* I, const uint32_t* J, const double* w, uint64_t m, uint32_t n,
+                                       uint32_t* I_out, uint32_t* J_out, double* w_out, void* ws, size_t ws_bytes,
+                                       int num_sms, cudaStream_t s);
+cudaError_t launch_spmv_f64_iter(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x,
+                                 double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s,
+                                 const int* stop, bool partitioned);
+size_t pagerank_workspace_bytes(uint32_t n, uint64_t m, int num_sms);
+cudaError_t launch_pagerank(const uint32_t* offsets, const uint32_t* indices, const double* w, uint32_t n, uint64_t m,
+                            double damping, double tol, int max_iters, double* x, uint32_t* iterations, void* ws,
+                            size_t ws_bytes, int num_sms, cudaStream_t s);
 cudaError_t launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, int num_sms,
                               cudaStream_t s);
 

@@ -200,7 +200,9 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
                                                       const T* __restrict__ w, const T* __restrict__ x,
                                                       T* __restrict__ y, uint32_t n, uint64_t m,
                                                       const uint32_t* __restrict__ coords,
-                                                      uint32_t* __restrict__ tile_head, T* __restrict__ tile_tail) {
+                                                      uint32_t* __restrict__ tile_head, T* __restrict__ tile_tail,
+                                                      const int* stop) {
+    if (stop && *(volatile const int*)stop) return;
     __shared__ uint32_t s_end[kSpTile + 1];
     __shared__ T s_val[kSpTile];
     __shared__ SegValT<T> s_warp[kSpNT / 32];
@@ -257,7 +259,8 @@ __device__ __forceinline__ SegValT<T> block_seg_scan(SegValT<T> v, SegValT<T>* s
 template <typename T>
 __global__ void __launch_bounds__(kSpChunk) k_spmv_chunk_agg(const uint32_t* __restrict__ tile_head,
                                                              const T* __restrict__ tile_tail, uint64_t tiles,
-                                                             unsigned* chunk_flag, T* chunk_val) {
+                                                             unsigned* chunk_flag, T* chunk_val, const int* stop) {
+    if (stop && *(volatile const int*)stop) return;
     using SegVal = SegValT<T>;
     __shared__ SegVal s_w[33];
     const uint64_t t = (uint64_t)blockIdx.x * kSpChunk + threadIdx.x;
@@ -277,7 +280,8 @@ template <typename T>
 __global__ void __launch_bounds__(kSpChunk) k_spmv_carry(const uint32_t* __restrict__ tile_head,
                                                          const T* __restrict__ tile_tail, uint64_t tiles,
                                                          const unsigned* __restrict__ chunk_flag,
-                                                         const T* __restrict__ chunk_val, T* y) {
+                                                         const T* __restrict__ chunk_val, T* y, const int* stop) {
+    if (stop && *(volatile const int*)stop) return;
     using SegVal = SegValT<T>;
     __shared__ SegVal s_w[33];
     __shared__ T s_cin;
@@ -311,7 +315,8 @@ size_t spmv_workspace_bytes(uint32_t n, uint64_t m) {
 
 template <typename T>
 cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, const T* w, const T* x, T* y, uint32_t n,
-                          uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s) {
+                          uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s, const int* stop = nullptr,
+                          bool partitioned = false) {
     if (n == 0) return cudaSuccess;
     if (ws_bytes < spmv_workspace_bytes(n, m)) return cudaErrorInvalidValue;
     const uint64_t tiles = ceil_div((uint64_t)n + m, kSpTile);
@@ -323,14 +328,17 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
     T* tile_tail = reinterpret_cast<T*>(p + 2 * arr);
     unsigned* chunk_flag = reinterpret_cast<unsigned*>(p + 3 * arr);
     T* chunk_val = reinterpret_cast<T*>(p + 3 * arr + ((chunks + 1) * 4 + 15) / 16 * 16);
-    k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
+    if (!partitioned)  // coords depend on the structure only: iterative callers compute them once
+        k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
     // (A persistent variant with a 128 KB shared-memory copy of the hub prefix of x
     // was measured slower at c2/c3: the occupancy it costs outweighs the hits.)
     k_spmv_merge<T><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head,
-                                                      tile_tail);
+                                                      tile_tail, stop);
     if (tiles > 1) {
-        k_spmv_chunk_agg<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val);
-        k_spmv_carry<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val, y);
+        k_spmv_chunk_agg<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val,
+                                                                 stop);
+        k_spmv_carry<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val, y,
+                                                             stop);
     }
     return cudaGetLastError();
 }
@@ -343,6 +351,12 @@ cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const 
 cudaError_t launch_spmv_f64(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x,
                             double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s) {
     return launch_spmv_t<double>(offsets, indices, w, x, y, n, m, ws, ws_bytes, s);
+}
+
+cudaError_t launch_spmv_f64_iter(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x,
+                                 double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s,
+                                 const int* stop, bool partitioned) {
+    return launch_spmv_t<double>(offsets, indices, w, x, y, n, m, ws, ws_bytes, s, stop, partitioned);
 }
 
 }  // namespace boba

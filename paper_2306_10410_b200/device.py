@@ -98,6 +98,40 @@ def degrees(I: torch.Tensor, n: int) -> torch.Tensor:
     return deg
 
 
+def total_degrees(I: torch.Tensor, J: torch.Tensor, n: int) -> torch.Tensor:
+    """reference graph.py:297-300 (in + out degree, uint32 counts)."""
+    deg = torch.empty(max(n, 1), dtype=ID, device=I.device)[:n]
+    N.check(N.lib.boba_total_degrees(_p(I), _p(J), I.numel(), n, _p(deg), _s()))
+    return deg
+
+
+def degree_order(I: torch.Tensor, J: torch.Tensor, n: int, hub: bool = False):
+    """reference ordering.py:160-164 (hub=False) / 167-176 (hub=True) ->
+    (order, label)."""
+    m = I.numel()
+    order = torch.empty(max(n, 1), dtype=ID, device=I.device)[:n]
+    label = torch.empty(max(n, 1), dtype=ID, device=I.device)[:n]
+    ws = _ws(N.lib.boba_degree_order_workspace_size(m, n), I.device)
+    fn = N.lib.boba_hub_order if hub else N.lib.boba_degree_order
+    N.check(fn(_p(I), _p(J), m, n, _p(order), _p(label), _p(ws), ws.numel(), _s()))
+    return order, label
+
+
+def sort_coo_by_destination(I: torch.Tensor, J: torch.Tensor, n: int, weights: torch.Tensor | None = None):
+    """reference graph.py:303-307: stable sort of the edges by J ->
+    (I_out, J_out, weights_out|None)."""
+    m = I.numel()
+    Io, Jo = torch.empty_like(I), torch.empty_like(J)
+    w_out = None
+    if weights is not None:
+        weights = weights.to(torch.float64).contiguous()
+        w_out = torch.empty(m, dtype=torch.float64, device=I.device)
+    ws = _ws(N.lib.boba_sort_coo_by_destination_workspace_size(m, n), I.device)
+    N.check(N.lib.boba_sort_coo_by_destination(_p(I), _p(J), _p(weights), m, n, _p(Io), _p(Jo), _p(w_out), _p(ws),
+                                               ws.numel(), _s()))
+    return Io, Jo, w_out
+
+
 def coo_to_csr(I2: torch.Tensor, J2: torch.Tensor, n: int, weights: torch.Tensor | None = None,
                row_counts: torch.Tensor | None = None):
     """Phase 4 (reference graph.py:253-277, _parallel.py:55-88) ->
@@ -134,6 +168,23 @@ def spmv(offsets: torch.Tensor, indices: torch.Tensor, x: torch.Tensor,
     fn = N.lib.boba_spmv_f64 if f64 else N.lib.boba_spmv
     N.check(fn(_p(offsets), _p(indices), _p(weights), _p(x), _p(y), n, m, _p(ws), ws.numel(), _s()))
     return y
+
+
+def pagerank(offsets: torch.Tensor, indices: torch.Tensor, weights: torch.Tensor | None = None,
+             damping: float = 0.85, tol: float = 1e-6, max_iters: int = 100):
+    """reference kernels.py:57-107 on a forward CSR -> (x float64, iterations
+    as a 1-element uint32 device tensor; no host synchronisation)."""
+    n = offsets.numel() - 1
+    m = indices.numel()
+    dev = offsets.device
+    if weights is not None:
+        weights = weights.to(torch.float64).contiguous()
+    x = torch.empty(max(n, 1), dtype=torch.float64, device=dev)[:n]
+    iters = torch.zeros(1, dtype=ID, device=dev)
+    ws = _ws(N.lib.boba_pagerank_workspace_size(n, m), dev)
+    N.check(N.lib.boba_pagerank(_p(offsets), _p(indices), _p(weights), n, m, float(damping), float(tol),
+                                int(max_iters), _p(x), _p(iters), _p(ws), ws.numel(), _s()))
+    return x, iters
 
 
 def spmv_workspace(n: int, m: int, device) -> torch.Tensor:

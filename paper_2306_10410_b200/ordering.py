@@ -10,10 +10,12 @@ Drop-in for the hot-path part of ``pkg/src/boba/ordering.py``:
   ``thread_hint`` None/1 the reference's racy loop is single threaded and
   therefore exact, so the deterministic kernel is used for that case.
 * ``boba_sequential`` reference ordering.py:59-96 -- same permutation.
+* ``degree_order`` / ``hub_order`` reference ordering.py:160-176 -- total
+  degrees by atomics, then a stable radix sort of the ids by degree key.
 * ``compute_ordering`` reference ordering.py:334-356 for the methods on the
-  path ("boba", "boba-relaxed") and the trivial baselines the bench pairs
-  with it ("random" = numpy PCG64 permutation exactly as the reference,
-  "identity").
+  path ("boba", "boba-relaxed"), the degree baselines ("degree", "hub") and
+  the trivial ones ("random" = numpy PCG64 permutation exactly as the
+  reference, "identity").  "rcm" (scipy on a symmetrised CSR) is out of scope.
 * ``BobaOrder`` reference ordering.py:273-290 (scikit-learn transformer).
 """
 
@@ -27,11 +29,12 @@ from . import _host
 from .graph import INDEX_DTYPE, CooGraph, Permutation, apply_permutation
 from .validation import check_coo
 
-__all__ = ["RANK_UNSET", "boba_sequential", "boba_parallel", "random_order", "identity_order",
-           "compute_ordering", "BobaOrder", "RandomOrder", "IdentityOrder", "ORDERING_CHOICES"]
+__all__ = ["RANK_UNSET", "boba_sequential", "boba_parallel", "random_order", "identity_order", "degree_order",
+           "hub_order", "compute_ordering", "BobaOrder", "RandomOrder", "IdentityOrder", "DegreeOrder", "HubOrder",
+           "ORDERING_CHOICES"]
 
 RANK_UNSET = _host.RANK_UNSET
-ORDERING_CHOICES = ("random", "boba", "boba-relaxed", "identity")
+ORDERING_CHOICES = ("random", "boba", "boba-relaxed", "degree", "hub", "identity")
 _MODES = ("deterministic", "relaxed")
 
 
@@ -61,6 +64,20 @@ def identity_order(n: int) -> Permutation:
     return Permutation.identity(n)
 
 
+def degree_order(g) -> Permutation:
+    """Total degree descending, ties by ascending id (reference
+    ordering.py:160-164, np.lexsort((arange(n), -deg)))."""
+    order, label = _host.degree_order(g.I, g.J, int(g.n))
+    return Permutation(order, label)
+
+
+def hub_order(g) -> Permutation:
+    """Vertices of above-mean total degree first by descending degree (ties
+    by id), the rest after them in id order (reference ordering.py:167-176)."""
+    order, label = _host.degree_order(g.I, g.J, int(g.n), hub=True)
+    return Permutation(order, label)
+
+
 def compute_ordering(g, method: str, seed: int = 0, mode: str = "deterministic",
                      thread_hint: int | None = None) -> Permutation:
     """Dispatch by method name (reference ordering.py:334-356)."""
@@ -70,9 +87,13 @@ def compute_ordering(g, method: str, seed: int = 0, mode: str = "deterministic",
         return boba_parallel(g, mode=mode, thread_hint=thread_hint)
     if method == "boba-relaxed":
         return boba_parallel(g, mode="relaxed", thread_hint=thread_hint)
+    if method == "degree":
+        return degree_order(g)
+    if method == "hub":
+        return hub_order(g)
     if method == "identity":
         return identity_order(g.n)
-    if method in ("degree", "hub", "rcm"):
+    if method == "rcm":
         raise ValueError(f"ordering method {method!r} is outside the B200 hot path; use the reference package")
     raise ValueError(f"unknown ordering method: {method!r}")
 
@@ -118,3 +139,17 @@ class RandomOrder(_Reorderer):
 class IdentityOrder(_Reorderer):
     def _permutation(self, X):
         return identity_order(X.n)
+
+
+class DegreeOrder(_Reorderer):
+    """Descending total-degree transformer (reference ordering.py:303-307)."""
+
+    def _permutation(self, X):
+        return degree_order(X)
+
+
+class HubOrder(_Reorderer):
+    """Hubs-first transformer (reference ordering.py:310-314)."""
+
+    def _permutation(self, X):
+        return hub_order(X)

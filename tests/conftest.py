@@ -41,7 +41,7 @@ class GoldenSet:
             out[k] = v[p[i]:p[i + 1]]
         out["n"] = int(out["n"][0])
         if not int(out.pop("weighted")[0]):
-            out["w"] = out["w2"] = out["w2_raw"] = None
+            out["w"] = out["w2"] = out["w2_raw"] = out["w_sd"] = None
         return out
 
     def __iter__(self):

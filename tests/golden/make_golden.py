@@ -59,10 +59,17 @@ def run_ref(g: CooGraph, x=None):
                offsets=csr.offsets, indices=csr.indices, x=x, y=y,
                deg=boba.degrees(g), offsets_raw=raw.offsets, indices_raw=raw.indices,
                y_raw=boba.spmv_pull(raw, x),
-               weighted=np.array([int(g.weights is not None)]))
+               weighted=np.array([int(g.weights is not None)]),
+               tdeg=boba.total_degrees(g), deg_order=boba.degree_order(g).order,
+               hub_order=boba.hub_order(g).order)
+    out["pr"], it = boba.pagerank(raw, return_iterations=True)
+    out["pr_iters"] = np.array([it])
+    sd = boba.sort_coo_by_destination(g)
+    out["I_sd"], out["J_sd"] = sd.I, sd.J
     if g.weights is not None:
         out["w2"] = csr.weights
         out["w2_raw"] = raw.weights
+        out["w_sd"] = sd.weights
     return out
 
 

@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
 
 RANK_UNSET = np.iinfo(np.int64).max
 SPMV_RTOL = 1e-5
+PR_RTOL = 1e-10   # fp64 PageRank vs the reference: differs only in summation order
 
 
 @pytest.fixture(scope="module")
@@ -50,6 +51,18 @@ def run_case(bb, c):
     np.testing.assert_allclose(y, c["y"], rtol=1e-12, atol=1e-12)
     y0 = bb.spmv_pull(raw, c["x"])
     np.testing.assert_allclose(y0, c["y_raw"], rtol=1e-12, atol=1e-12)
+    # §8f: PageRank on the direct CSR (fp64; tolerance: summation order only)
+    x, it = bb.pagerank(raw, return_iterations=True)
+    assert it == c["pr_iters"][0], "pagerank iterations"
+    np.testing.assert_allclose(x, c["pr"], rtol=PR_RTOL, atol=1e-14)
+    # §8f: degree / hub orderings and the destination sort
+    assert np.array_equal(bb.total_degrees(g), c["tdeg"]), "total_degrees"
+    assert np.array_equal(bb.degree_order(g).order, c["deg_order"]), "degree_order"
+    assert np.array_equal(bb.hub_order(g).order, c["hub_order"]), "hub_order"
+    sd = bb.sort_coo_by_destination(g)
+    assert np.array_equal(sd.I, c["I_sd"]) and np.array_equal(sd.J, c["J_sd"]), "sort_coo_by_destination"
+    if c["w"] is not None:
+        assert np.array_equal(sd.weights, c["w_sd"])
 
 
 def test_known_answers(bb, kat):
@@ -285,3 +298,81 @@ def test_host_pipeline_matches_device(dev):
     assert np.array_equal(off, pipe.offsets[: n + 1].cpu().numpy().view(np.uint32))
     assert np.array_equal(idx, pipe.indices[:m].cpu().numpy().view(np.uint32))
     hp.close()
+
+
+@pytest.mark.parametrize("scale,ef", [(12, 16), (20, 16)])
+def test_degree_orders_and_destination_sort_vs_oracle(bb, dev, scale, ef):
+    """R-MAT (heavy ties in degree) through the C ABI vs the oracle."""
+    import torch
+
+    I, J = dev.generate_rmat(scale, ef, seed=5)
+    n = 1 << scale
+    hI, hJ = to_np(I), to_np(J)
+    deg = dev.total_degrees(I, J, n)
+    assert np.array_equal(to_np(deg), oracle.total_degrees(hI, hJ, n))
+    for hub in (False, True):
+        order, label = dev.degree_order(I, J, n, hub=hub)
+        want = oracle.degree_order(hI, hJ, n, hub=hub)
+        assert np.array_equal(to_np(order), want)
+        assert np.array_equal(to_np(label), oracle.label_from_order(want))
+    w = torch.rand(I.numel(), dtype=torch.float64, device=I.device)
+    Io, Jo, wo = dev.sort_coo_by_destination(I, J, n, w)
+    eI, eJ, ew = oracle.sort_coo_by_destination(hI, hJ, n, w.cpu().numpy())
+    assert np.array_equal(to_np(Io), eI) and np.array_equal(to_np(Jo), eJ)
+    assert np.array_equal(wo.cpu().numpy(), ew)
+    Io, Jo, _ = dev.sort_coo_by_destination(I, J, n)
+    assert np.array_equal(to_np(Io), eI) and np.array_equal(to_np(Jo), eJ)
+
+
+def test_degree_order_edge_cases(bb):
+    g = bb.CooGraph(5, [], [])
+    assert bb.degree_order(g).order.tolist() == [0, 1, 2, 3, 4]
+    assert bb.hub_order(g).order.tolist() == [0, 1, 2, 3, 4]
+    g = bb.CooGraph(1, [0], [0])
+    assert bb.degree_order(g).order.tolist() == [0]
+    g = bb.CooGraph(0, [], [])
+    assert bb.degree_order(g).order.size == 0
+    star = bb.CooGraph(5, [0, 0, 0, 0], [1, 2, 3, 4])
+    assert bb.compute_ordering(star, "degree").order.tolist() == [0, 1, 2, 3, 4]
+    assert bb.compute_ordering(star, "hub").order.tolist() == [0, 1, 2, 3, 4]
+    g = bb.CooGraph(4, [3, 3, 2], [1, 1, 3])
+    assert bb.compute_ordering(g, "degree").order.tolist() == [3, 1, 2, 0]
+    assert bb.DegreeOrder().fit(g).permutation_.order.tolist() == [3, 1, 2, 0]
+    assert bb.HubOrder().fit(g).permutation_.order.tolist() == [3, 1, 0, 2]
+    sd = bb.sort_coo_by_destination(bb.CooGraph(4, [0, 1, 2, 3], [2, 0, 2, 0], [1.0, 2.0, 3.0, 4.0]))
+    assert sd.I.tolist() == [1, 3, 0, 2] and sd.weights.tolist() == [2.0, 4.0, 1.0, 3.0]
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_pagerank_rmat_vs_oracle(bb, dev, weighted):
+    import torch
+
+    scale = 16
+    I, J = dev.generate_rmat(scale, 8, seed=3)
+    n = 1 << scale
+    w = torch.rand(I.numel(), dtype=torch.float64, device=I.device) if weighted else None
+    off, idx, w2 = dev.coo_to_csr(I, J, n, w)
+    x, it = dev.pagerank(off, idx, w2)
+    ho, hi = to_np(off), to_np(idx)
+    ex, eit = oracle.pagerank(ho, hi, n, None if w2 is None else w2.cpu().numpy())
+    assert int(it.cpu()[0]) == eit
+    np.testing.assert_allclose(x.cpu().numpy(), ex, rtol=PR_RTOL, atol=1e-15)
+    assert abs(x.sum().item() - 1.0) < 1e-9
+    x2, _ = dev.pagerank(off, idx, w2)
+    assert torch.equal(x, x2), "PageRank must be bitwise deterministic"
+
+
+def test_pagerank_edge_cases(bb):
+    g = bb.CooGraph(3, [0, 1], [1, 2])
+    csr = bb.coo_to_csr(g)
+    x, it = bb.pagerank(csr, max_iters=0, return_iterations=True)
+    assert it == 0 and np.allclose(x, 1 / 3)
+    x, it = bb.pagerank(csr, max_iters=1, return_iterations=True)
+    ex, eit = oracle.pagerank(csr.offsets, csr.indices, 3, max_iters=1)
+    assert it == eit == 1 and np.allclose(x, ex, rtol=1e-14)
+    x = bb.pagerank(bb.coo_to_csr(bb.CooGraph(4, [], [])))
+    assert np.allclose(x, 0.25)
+    assert bb.pagerank(bb.coo_to_csr(bb.CooGraph(0, [], []))).size == 0
+    for d in (0.0, 1.0, -0.5):
+        with pytest.raises(ValueError):
+            bb.pagerank(csr, damping=d)

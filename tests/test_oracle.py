@@ -44,6 +44,17 @@ def check_case(c):
     assert np.array_equal(oracle.degrees(I, n), c["deg"])
     y = oracle.spmv_pull(off, idx, c["x"], w2)
     np.testing.assert_allclose(y, c["y"], rtol=1e-12, atol=1e-12)
+    # the orderings and the edge sort beside BOBA
+    assert np.array_equal(oracle.total_degrees(I, J, n), c["tdeg"])
+    assert np.array_equal(oracle.degree_order(I, J, n), c["deg_order"])
+    assert np.array_equal(oracle.degree_order(I, J, n, hub=True), c["hub_order"])
+    x, it = oracle.pagerank(off0, idx0, n, w0)
+    assert it == c["pr_iters"][0]
+    np.testing.assert_allclose(x, c["pr"], rtol=1e-10, atol=1e-14)
+    Is, Js, ws = oracle.sort_coo_by_destination(I, J, n, c["w"])
+    assert np.array_equal(Is, c["I_sd"]) and np.array_equal(Js, c["J_sd"])
+    if c["w"] is not None:
+        assert np.array_equal(ws, c["w_sd"])
 
 
 def test_known_answers(kat):
