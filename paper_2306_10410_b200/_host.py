@@ -8,6 +8,8 @@ widens the results back to int64 on the device before a single D2H copy.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -22,7 +24,9 @@ def _dev():
 
 def to_device_ids(a, bound: int, name: str = "ids") -> torch.Tensor:
     arr = np.ascontiguousarray(a, dtype=np.int64)
-    t = torch.from_numpy(arr).to(_dev())
+    with warnings.catch_warnings():   # frozen (read-only) container arrays: only read, copied to the device
+        warnings.simplefilter("ignore", UserWarning)
+        t = torch.from_numpy(arr).to(_dev())
     return D.narrow_ids(t, bound, name)
 
 
