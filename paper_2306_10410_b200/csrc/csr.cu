@@ -291,13 +291,21 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
     return cudaGetLastError();
 }
 
+// RB is the widest digit the pass supports; the ranking spends one ballot per
+// bit of RB, so narrower passes (7 or <= 6 bits) use a narrower instantiation.
 template <int RB, int NT, int IPT, int MINB>
 cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits, uint32_t* H,
                        unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
                        int num_sms, cudaStream_t s, uint32_t* row_starts, bool skip_up) {
-    return radix_pass_op<RB, NT, IPT, MINB, DigitShift>(kin, vin, m, DigitShift{shift, (1u << bits) - 1u}, bits, H,
-                                                        scan_status, counter, kout, vout, num_sms, s, row_starts,
-                                                        skip_up);
+    const DigitShift op{shift, (1u << bits) - 1u};
+    if (RB == 8 && bits <= 6)
+        return radix_pass_op<6, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
+                                                           num_sms, s, row_starts, skip_up);
+    if (RB == 8 && bits == 7)
+        return radix_pass_op<7, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
+                                                           num_sms, s, row_starts, skip_up);
+    return radix_pass_op<RB, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
+                                                        num_sms, s, row_starts, skip_up);
 }
 
 cudaError_t dispatch_pass(Variant v, const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits,

@@ -43,10 +43,8 @@ struct RadixCfg {
     static constexpr int NW = NT / 32;
     static constexpr int TILE = NT * IPT;
     static constexpr int BPT = B >= NT ? B / NT : 1;              // digits per thread in the scans
-    static constexpr int SUB = 1;  // measured: 2 or 4 chains cost more in registers than they gain  // independent counter chains per warp
-    static constexpr int VW = NW * SUB;                              // "virtual warps" (warp, chain)
-    static constexpr int HIST_BYTES = (VW * B * 2 + 15) / 16 * 16;  // 16-bit counters per virtual warp
-    static constexpr int STAGE_BYTES = TILE * 8;                    // staged keys + payloads
+    static constexpr int HIST_BYTES = (NW * B * 2 + 15) / 16 * 16;  // 16-bit counters per warp
+    static constexpr int STAGE_BYTES = TILE * 8;                    // staged (key, payload) pairs
     static constexpr int RAW_BYTES = TILE * 4;                      // payloads prefetched by cp.async
     static constexpr size_t SMEM = (size_t)HIST_BYTES + STAGE_BYTES + RAW_BYTES + 2 * B * 4;  // + s_off, s_glob
     static_assert(TILE < 65536, "16-bit counters and packed ranks");
@@ -124,6 +122,44 @@ __global__ void __launch_bounds__(kScanTileNT) k_scan_u32(uint32_t* data, uint64
 }
 
 // ----------------------------------------------------------- downsweep ---
+// Ranks the warp's IPT 32-item slots: peers (same digit) via one ballot per
+// digit bit, the lowest peer bumps the warp's 16-bit counter.  FULL: every
+// item of the tile is valid (all tiles but the last), no per-item checks.
+template <int RB, int IPT, bool FULL, typename Op>
+__device__ __forceinline__ void rank_slots(const uint32_t (&key)[IPT], uint32_t (&rank)[IPT], uint16_t* wh,
+                                           Op op, uint64_t wslot, uint64_t m) {
+    const unsigned lane = lane_id(), lt = lanemask_lt();
+#pragma unroll
+    for (int i = 0; i < IPT; i++) {
+        const bool ok = FULL || wslot + (uint64_t)i * 32 + lane < m;
+        const uint32_t d = op(key[i]);
+        unsigned peers = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, ok);
+        // peers &= lanes whose digit bit b equals mine, for every bit b:
+        // one predicate test, one ballot and one predicated AND per bit.
+#pragma unroll
+        for (int b = 0; b < RB; b++) {  // bits >= `bits` are zero in every lane: no effect
+            asm("{\n\t"
+                ".reg .pred p;\n\t"
+                ".reg .b32 bb;\n\t"
+                "and.b32 bb, %1, %2;\n\t"
+                "setp.ne.u32 p, bb, 0;\n\t"
+                "vote.sync.ballot.b32 bb, p, 0xffffffff;\n\t"
+                "@!p not.b32 bb, bb;\n\t"
+                "and.b32 %0, %0, bb;\n\t"
+                "}"
+                : "+r"(peers)
+                : "r"(d), "r"(1u << b));
+        }
+        const unsigned below = peers & lt;
+        uint32_t pre = 0;
+        if (ok) pre = wh[d];
+        __syncwarp();
+        if (ok && below == 0) wh[d] = (uint16_t)(pre + __popc(peers));
+        rank[i] = ok ? pre + __popc(below) : 0xFFFFFFFFu;
+        __syncwarp();
+    }
+}
+
 template <int RB, int NT, int IPT, int MINB, typename Op>
 __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in, uint64_t m,
@@ -136,9 +172,8 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     constexpr int B = C::B, NW = C::NW, TILE = C::TILE, BPT = C::BPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint16_t* s_hist = reinterpret_cast<uint16_t*>(smem_raw);                  // NW x B warp counters
-    uint32_t* s_key = reinterpret_cast<uint32_t*>(smem_raw + C::HIST_BYTES);   // TILE staged keys
-    uint32_t* s_val = s_key + TILE;                                            // TILE staged payloads
-    uint32_t* s_raw = s_val + TILE;                                            // TILE payloads, input order
+    uint2* s_kv = reinterpret_cast<uint2*>(smem_raw + C::HIST_BYTES);          // TILE staged (key, payload)
+    uint32_t* s_raw = reinterpret_cast<uint32_t*>(s_kv + TILE);                // TILE payloads, input order
     uint32_t* s_off = s_raw + TILE;                                            // B: tile-local digit offsets
     uint32_t* s_glob = s_off + B;                                              // B: global position - s_off
     __shared__ uint32_t s_scan[NW + 1];
@@ -150,7 +185,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     const uint64_t wslot = tile_base + (uint64_t)warp * 32 * IPT;
     const bool full = tile_base + TILE <= m;
 
-    for (int i = threadIdx.x; i < C::VW * B / 2; i += NT) reinterpret_cast<uint32_t*>(s_hist)[i] = 0;
+    for (int i = threadIdx.x; i < NW * B / 2; i += NT) reinterpret_cast<uint32_t*>(s_hist)[i] = 0;
     // Prefetch this warp's payload run (IPT*32 words) into shared memory with
     // cp.async; it lands while the warp ranks its keys.
     uint32_t* wraw = s_raw + warp * 32 * IPT;
@@ -186,48 +221,15 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
         }
     }
     __syncthreads();
-    // A warp's IPT slots form SUB independent chains of consecutive slots, each
-    // with its own counters (a "virtual warp"), so SUB read-modify-write chains
-    // through shared memory proceed in parallel.
-    constexpr int SUB = C::SUB, SPC = IPT / SUB;
-    uint16_t* wh = s_hist + warp * SUB * B;
-    const unsigned lt = lanemask_lt();
-#pragma unroll
-    for (int si = 0; si < SPC; si++) {
-#pragma unroll
-        for (int c = 0; c < SUB; c++) {
-            const int i = c * SPC + si;
-            const bool ok = full || wslot + (uint64_t)i * 32 + lane < m;
-            const uint32_t d = op(key[i]);
-            unsigned peers = full ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, ok);
-            // peers &= lanes whose digit bit b equals mine, for every bit b:
-            // one predicate test, one ballot and one predicated AND per bit.
-#pragma unroll
-            for (int b = 0; b < RB; b++) {  // bits >= `bits` are zero in every lane: no effect
-                asm("{\n\t"
-                    ".reg .pred p;\n\t"
-                    ".reg .b32 bb;\n\t"
-                    "and.b32 bb, %1, %2;\n\t"
-                    "setp.ne.u32 p, bb, 0;\n\t"
-                    "vote.sync.ballot.b32 bb, p, 0xffffffff;\n\t"
-                    "@!p not.b32 bb, bb;\n\t"
-                    "and.b32 %0, %0, bb;\n\t"
-                    "}"
-                    : "+r"(peers)
-                    : "r"(d), "r"(1u << b));
-            }
-            const unsigned below = peers & lt;
-            uint16_t* ch = wh + c * B;
-            uint32_t pre = 0;
-            if (ok) pre = ch[d];
-            __syncwarp();
-            if (ok && below == 0) ch[d] = (uint16_t)(pre + __popc(peers));
-            rank[i] = ok ? pre + __popc(below) : 0xFFFFFFFFu;
-        }
-        __syncwarp();
-    }
+    uint16_t* wh = s_hist + warp * B;
+    if (full)
+        rank_slots<RB, IPT, true>(key, rank, wh, op, wslot, m);
+    else
+        rank_slots<RB, IPT, false>(key, rank, wh, op, wslot, m);
     __syncthreads();
-    // Per-digit exclusive scan across warps, then across digits (tile offsets).
+    // Per digit: tile offset (block scan of the digit totals), then every
+    // warp's counter becomes tile offset + the digit's count in earlier warps,
+    // so an item's tile rank is one shared load away.
     uint32_t cnt[BPT];
 #pragma unroll
     for (int b = 0; b < BPT; b++) {
@@ -235,11 +237,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
         uint32_t run = 0;
         if (d < nb) {
 #pragma unroll
-            for (int w = 0; w < C::VW; w++) {
-                const uint32_t c = s_hist[w * B + d];
-                s_hist[w * B + d] = (uint16_t)run;
-                run += c;
-            }
+            for (int w = 0; w < NW; w++) run += s_hist[w * B + d];
         }
         cnt[b] = run;
     }
@@ -255,36 +253,36 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
             if (d < nb) {
                 s_off[d] = ex;
                 s_glob[d] = __ldg(H + (uint64_t)d * tiles + tile) - ex;
+                uint32_t run = ex;
+#pragma unroll
+                for (int w = 0; w < NW; w++) {
+                    const uint32_t c = s_hist[w * B + d];
+                    s_hist[w * B + d] = (uint16_t)run;
+                    run += c;
+                }
             }
             ex += cnt[b];
         }
     }
     __syncthreads();
-#pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        if (rank[i] != 0xFFFFFFFFu) {
-            const uint32_t d = op(key[i]);
-            rank[i] += s_off[d] + wh[(i / SPC) * B + d];
-        }
-    }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
         if (rank[i] != 0xFFFFFFFFu) {
-            s_key[rank[i]] = key[i];
-            s_val[rank[i]] = vals_in ? wraw[i * 32 + lane] : (uint32_t)(wslot + (uint64_t)i * 32 + lane);
+            const uint32_t r = rank[i] + wh[op(key[i])];
+            s_kv[r] = make_uint2(key[i], vals_in ? wraw[i * 32 + lane] : (uint32_t)(wslot + (uint64_t)i * 32 + lane));
         }
     }
     __syncthreads();
     const uint64_t rem = m - tile_base;
     const int items = rem < (uint64_t)TILE ? (int)rem : TILE;
     for (int j = threadIdx.x; j < items; j += NT) {
-        const uint32_t k = s_key[j];
-        const uint32_t d = op(k);
+        const uint2 kv = s_kv[j];
+        const uint32_t d = op(kv.x);
         const uint32_t g = s_glob[d] + (uint32_t)j;
-        if (keys_out) keys_out[g] = k;
-        vals_out[g] = s_val[j];
+        if (keys_out) keys_out[g] = kv.x;
+        vals_out[g] = kv.y;
         if (row_starts) {
             // Last (most significant) pass: the output is sorted by key, and this
             // tile's run for digit d is a contiguous segment of it.  A key change
@@ -292,9 +290,9 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
             // continue the previous run, so it only lowers the slot.  Slots start
             // at 0xFFFFFFFF; empty rows are filled by a suffix-min afterwards.
             if (j == (int)s_off[d])
-                atomicMin(row_starts + k, g);
-            else if (s_key[j - 1] != k)
-                row_starts[k] = g;
+                atomicMin(row_starts + kv.x, g);
+            else if (s_kv[j - 1].x != kv.x)
+                row_starts[kv.x] = g;
         }
     }
 }
