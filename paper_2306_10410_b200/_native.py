@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libboba_b200.so")
+LIB_PATH = os.environ.get("BOBA_LIB_PATH") or os.path.join(_HERE, "libboba_b200.so")  # override: experiments only
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "boba_b200.h")
 
 BOBA_OK, BOBA_EINVAL, BOBA_ECUDA, BOBA_ERANGE, BOBA_ENOMEM = 0, 1, 2, 3, 4

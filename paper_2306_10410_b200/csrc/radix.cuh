@@ -18,6 +18,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef RADIX_SUB
+#define RADIX_SUB 2
+#endif
+
 namespace boba {
 
 // Digit extractors: the LSD passes use a shift/mask digit; the multi-GPU row
@@ -43,7 +47,9 @@ struct RadixCfg {
     static constexpr int NW = NT / 32;
     static constexpr int TILE = NT * IPT;
     static constexpr int BPT = B >= NT ? B / NT : 1;              // digits per thread in the scans
-    static constexpr int HIST_BYTES = (NW * B * 2 + 15) / 16 * 16;  // 16-bit counters per warp
+    static constexpr int SUB = RADIX_SUB;                            // independent counter chains per warp
+    static constexpr int VW = NW * SUB;                              // "virtual warps" (warp, chain)
+    static constexpr int HIST_BYTES = (VW * B * 2 + 15) / 16 * 16;  // 16-bit counters per virtual warp
     static constexpr int STAGE_BYTES = TILE * 8;                    // staged (key, payload) pairs
     static constexpr int RAW_BYTES = TILE * 4;                      // payloads prefetched by cp.async
     static constexpr size_t SMEM = (size_t)HIST_BYTES + STAGE_BYTES + RAW_BYTES + 2 * B * 4;  // + s_off, s_glob
@@ -125,12 +131,19 @@ __global__ void __launch_bounds__(kScanTileNT) k_scan_u32(uint32_t* data, uint64
 // Ranks the warp's IPT 32-item slots: peers (same digit) via one ballot per
 // digit bit, the lowest peer bumps the warp's 16-bit counter.  FULL: every
 // item of the tile is valid (all tiles but the last), no per-item checks.
-template <int RB, int IPT, bool FULL, typename Op>
+template <int RB, int IPT, int SUB, bool FULL, typename Op>
 __device__ __forceinline__ void rank_slots(const uint32_t (&key)[IPT], uint32_t (&rank)[IPT], uint16_t* wh,
                                            Op op, uint64_t wslot, uint64_t m) {
+    constexpr int B = 1 << RB, SPC = IPT / SUB;
     const unsigned lane = lane_id(), lt = lanemask_lt();
+    // SUB chains of consecutive slots, each with its own counters, advance
+    // together so their shared-memory read-modify-write latencies overlap.
 #pragma unroll
-    for (int i = 0; i < IPT; i++) {
+    for (int si = 0; si < SPC; si++) {
+#pragma unroll
+    for (int c = 0; c < SUB; c++) {
+        const int i = c * SPC + si;
+        uint16_t* ch = wh + c * B;
         const bool ok = FULL || wslot + (uint64_t)i * 32 + lane < m;
         const uint32_t d = op(key[i]);
         unsigned peers = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, ok);
@@ -152,10 +165,11 @@ __device__ __forceinline__ void rank_slots(const uint32_t (&key)[IPT], uint32_t 
         }
         const unsigned below = peers & lt;
         uint32_t pre = 0;
-        if (ok) pre = wh[d];
+        if (ok) pre = ch[d];
         __syncwarp();
-        if (ok && below == 0) wh[d] = (uint16_t)(pre + __popc(peers));
+        if (ok && below == 0) ch[d] = (uint16_t)(pre + __popc(peers));
         rank[i] = ok ? pre + __popc(below) : 0xFFFFFFFFu;
+    }
         __syncwarp();
     }
 }
@@ -185,7 +199,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     const uint64_t wslot = tile_base + (uint64_t)warp * 32 * IPT;
     const bool full = tile_base + TILE <= m;
 
-    for (int i = threadIdx.x; i < NW * B / 2; i += NT) reinterpret_cast<uint32_t*>(s_hist)[i] = 0;
+    for (int i = threadIdx.x; i < C::VW * B / 2; i += NT) reinterpret_cast<uint32_t*>(s_hist)[i] = 0;
     // Prefetch this warp's payload run (IPT*32 words) into shared memory with
     // cp.async; it lands while the warp ranks its keys.
     uint32_t* wraw = s_raw + warp * 32 * IPT;
@@ -221,11 +235,11 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
         }
     }
     __syncthreads();
-    uint16_t* wh = s_hist + warp * B;
+    uint16_t* wh = s_hist + warp * C::SUB * B;
     if (full)
-        rank_slots<RB, IPT, true>(key, rank, wh, op, wslot, m);
+        rank_slots<RB, IPT, C::SUB, true>(key, rank, wh, op, wslot, m);
     else
-        rank_slots<RB, IPT, false>(key, rank, wh, op, wslot, m);
+        rank_slots<RB, IPT, C::SUB, false>(key, rank, wh, op, wslot, m);
     __syncthreads();
     // Per digit: tile offset (block scan of the digit totals), then every
     // warp's counter becomes tile offset + the digit's count in earlier warps,
@@ -237,7 +251,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
         uint32_t run = 0;
         if (d < nb) {
 #pragma unroll
-            for (int w = 0; w < NW; w++) run += s_hist[w * B + d];
+            for (int w = 0; w < C::VW; w++) run += s_hist[w * B + d];
         }
         cnt[b] = run;
     }
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
                 s_glob[d] = __ldg(H + (uint64_t)d * tiles + tile) - ex;
                 uint32_t run = ex;
 #pragma unroll
-                for (int w = 0; w < NW; w++) {
+                for (int w = 0; w < C::VW; w++) {
                     const uint32_t c = s_hist[w * B + d];
                     s_hist[w * B + d] = (uint16_t)run;
                     run += c;
@@ -270,7 +284,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
         if (rank[i] != 0xFFFFFFFFu) {
-            const uint32_t r = rank[i] + wh[op(key[i])];
+            const uint32_t r = rank[i] + wh[(i / (IPT / C::SUB)) * B + op(key[i])];
             s_kv[r] = make_uint2(key[i], vals_in ? wraw[i * 32 + lane] : (uint32_t)(wslot + (uint64_t)i * 32 + lane));
         }
     }
