@@ -209,6 +209,77 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def spmv_speedup(D, I, J, pipe, n, m, k_iters, flush, stream, t_reorder=None, t_convert=None):
+    """e2e = (t_reorder + t_convert + k t_spmv) after BOBA vs
+    (t_convert + k t_spmv) on the randomly labelled input (reference bench.py
+    135-156: reorder_ms, convert_ms, kernel over the forward CSR, x = ones).
+    Times are CUDA-event medians with the L2 flushed before each sample."""
+    import ctypes
+
+    import torch
+
+    from paper_2306_10410_b200 import _native as N
+
+    x = torch.ones(n, dtype=torch.float32, device=I.device)
+    y = torch.empty(n, dtype=torch.float32, device=I.device)
+    spws = D.spmv_workspace(n, m, I.device)
+
+    def time_it(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    if t_reorder is None:
+        # phase times of the fused pipeline call, from its own events
+        ph = {"reorder": [], "convert": []}
+        for _ in range(4):
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            for e in evs:
+                e.record(stream)
+            arr = (ctypes.c_void_p * 5)(*[e.cuda_event for e in evs])
+            torch.cuda.synchronize()
+            flush.fill_(1)
+            N.check(N.lib.boba_reorder_to_csr_timed(
+                D._p(I), D._p(J), None, m, n, D._p(pipe.first), D._p(pipe.order), D._p(pipe.label),
+                D._p(pipe.I2), D._p(pipe.J2), D._p(pipe.offsets), D._p(pipe.indices), None, D._p(pipe.ws),
+                pipe.ws.numel(), D._s(), arr))
+            torch.cuda.synchronize()
+            ph["reorder"].append(evs[0].elapsed_time(evs[3]))
+            ph["convert"].append(evs[3].elapsed_time(evs[4]))
+        t_reorder = statistics.median(ph["reorder"][1:])
+        t_convert = statistics.median(ph["convert"][1:])
+    off_b, idx_b = pipe.offsets[: n + 1], pipe.indices[:m]
+    t_spmv_boba = time_it(lambda: [D.spmv(off_b, idx_b, x, out=y, ws=spws) for _ in range(k_iters)], 3) / k_iters
+    rnd = {}
+
+    def convert_random():
+        rnd["csr"] = D.coo_to_csr(I, J, n)
+
+    t_conv_rand = time_it(convert_random, 3)
+    off_r, idx_r, _ = rnd["csr"]
+    t_spmv_rand = time_it(lambda: [D.spmv(off_r, idx_r, x, out=y, ws=spws) for _ in range(k_iters)], 3) / k_iters
+    e2e_boba = t_reorder + t_convert + k_iters * t_spmv_boba
+    e2e_rand = t_conv_rand + k_iters * t_spmv_rand
+    return {
+        "n": n, "m": m, "iters": k_iters, "x": "ones",
+        "spmv_ms_boba": round(t_spmv_boba, 4), "spmv_ms_random": round(t_spmv_rand, 4),
+        "convert_ms_random": round(t_conv_rand, 4), "reorder_ms": round(t_reorder, 4),
+        "convert_ms_boba": round(t_convert, 4),
+        "e2e_ms_boba": round(e2e_boba, 4), "e2e_ms_random": round(e2e_rand, 4),
+        "e2e_speedup_boba_vs_random": round(e2e_rand / e2e_boba, 4),
+        "spmv_gflops_boba": round(2 * m / t_spmv_boba / 1e6, 1),
+    }
+
+
 # ----------------------------------------------------------------- GPU arm
 def run_ours(args):
     import torch
@@ -313,49 +384,27 @@ def run_ours(args):
     }
 
     # ---- SpMV e2e speedup: BOBA (reorder+convert+k SpMV) vs random labels (convert + k SpMV)
-    k_iters = SPMV_ITERS[cfg]
-    x = torch.ones(n, dtype=torch.float32, device=dev)
-    y = torch.empty(n, dtype=torch.float32, device=dev)
-    spws = D.spmv_workspace(n, m, dev)
-
-    def time_it(fn, reps):
-        fn()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(reps):
-            flush.fill_(1)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
-
-    off_b, idx_b = pipe.offsets[: n + 1], pipe.indices[:m]
-    t_spmv_boba = time_it(lambda: [D.spmv(off_b, idx_b, x, out=y, ws=spws) for _ in range(k_iters)], 3) / k_iters
-    rnd = {}
-
-    def convert_random():
-        rnd["csr"] = D.coo_to_csr(I, J, n)
-
-    t_conv_rand = time_it(convert_random, 3)
-    off_r, idx_r, _ = rnd["csr"]
-    t_spmv_rand = time_it(lambda: [D.spmv(off_r, idx_r, x, out=y, ws=spws) for _ in range(k_iters)], 3) / k_iters
     t_reorder = sum(statistics.mean(phase_ms[k]) for k in phase_names[:3])
     t_convert = statistics.mean(phase_ms["coo_to_csr"])
-    e2e_boba = t_reorder + t_convert + k_iters * t_spmv_boba
-    e2e_rand = t_conv_rand + k_iters * t_spmv_rand
-    spmv_info = {
-        "iters": k_iters, "x": "ones",
-        "spmv_ms_boba": round(t_spmv_boba, 4), "spmv_ms_random": round(t_spmv_rand, 4),
-        "convert_ms_random": round(t_conv_rand, 4), "reorder_ms": round(t_reorder, 4),
-        "convert_ms_boba": round(t_convert, 4),
-        "e2e_ms_boba": round(e2e_boba, 4), "e2e_ms_random": round(e2e_rand, 4),
-        "e2e_speedup_boba_vs_random": round(e2e_rand / e2e_boba, 4),
-        "spmv_gflops_boba": round(2 * m / t_spmv_boba / 1e6, 1),
-    }
-    del rnd
+    spmv_info = spmv_speedup(D, I, J, pipe, n, m, SPMV_ITERS[cfg], flush, stream, t_reorder, t_convert)
+    spmv_info["config"] = cfg
+    if cfg == "c2" and not args.no_spmv_c3:
+        # the SURVEY d1 headline pairing: the road-like grid (c3) with 100 SpMV iterations
+        del pipe
+        torch.cuda.empty_cache()
+        n3, m3 = graph_size("c3")
+        G0, G1 = D.generate_grid(CONFIGS["c3"][1]["rows"], CONFIGS["c3"][1]["cols"], dev)
+        lab3 = torch.from_numpy(oracle.random_labels(n3, LABEL_SEED).astype(np.int32)).to(dev)
+        I3, J3 = D.gather(lab3, G0), D.gather(lab3, G1)
+        del G0, G1, lab3
+        pipe3 = D.Pipeline(m3, n3, dev)
+        c3 = spmv_speedup(D, I3, J3, pipe3, n3, m3, SPMV_ITERS["c3"], flush, stream)
+        c3["config"] = "c3"
+        spmv_info = {"c2": spmv_info, "c3": c3,
+                     "headline": "c3 (SURVEY d1: grid, k = 100 SpMV iterations)"}
+        del pipe3, I3, J3
+        torch.cuda.empty_cache()
+        pipe = None
 
     # ---- end to end through the host-buffer C-ABI entry (pinned buffers)
     hI = torch.empty(m, dtype=torch.int32, pin_memory=True)
@@ -578,6 +627,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-spmv-c3", action="store_true", help="skip the c3 (grid, 100 SpMV) e2e comparison")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded pipeline even on 1 GPU")
     args = ap.parse_args()
     if args.impl == "reference":
