@@ -142,7 +142,7 @@ int boba_reorder_to_csr_timed(const uint32_t *I, const uint32_t *J, const double
                               double *weights_out, void *workspace, size_t workspace_bytes,
                               void *stream, void *const *events);
 
-/* --- Host-buffer pipeline (end to end, synchronous) ----------------------
+/* --- Host-buffer pipeline (end to end) ----------------------------------
  * A context owns device buffers for graphs up to (max_m, max_n) on the
  * current device plus a stream.  boba_ctx_reorder_to_csr_host copies I, J
  * host -> device, runs the fused pipeline and copies order, label, offsets
@@ -155,6 +155,17 @@ int boba_ctx_reorder_to_csr_host(boba_ctx *ctx, const uint32_t *I_host, const ui
                                  uint64_t m, uint32_t n, uint32_t *order_host, uint32_t *label_host,
                                  uint32_t *I2_host, uint32_t *J2_host, uint32_t *offsets_host,
                                  uint32_t *indices_host);
+/* Asynchronous form: enqueue one graph and return at once with *ticket.  A
+ * context has two buffer slots, so graph k+1's host->device copy and graph
+ * k's device->host copy overlap each other and the compute of either (the
+ * copies run on their own streams).  The caller keeps the host inputs intact,
+ * and does not read the host outputs, until boba_ctx_wait(ticket) returns.
+ * Host buffers should be pinned; pageable buffers serialise the copies. */
+int boba_ctx_submit_host(boba_ctx *ctx, const uint32_t *I_host, const uint32_t *J_host, uint64_t m,
+                         uint32_t n, uint32_t *order_host, uint32_t *label_host, uint32_t *I2_host,
+                         uint32_t *J2_host, uint32_t *offsets_host, uint32_t *indices_host,
+                         uint64_t *ticket);
+int boba_ctx_wait(boba_ctx *ctx, uint64_t ticket);
 
 /* --- Plumbing and input generators --------------------------------------- */
 /* int64 -> uint32 with the reference's range check (graph.py:99-106):

@@ -59,15 +59,28 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 }  // namespace
 
+// Host-buffer contexts: two buffer slots so that consecutive graphs overlap
+// (H2D of graph k+1 and D2H of graph k run on their own copy streams while
+// the compute stream works); the compute-internal arrays (first, I2, J2,
+// workspace) are shared because the compute stream serialises the graphs.
+struct boba_slot {
+    uint32_t *I = nullptr, *J = nullptr, *order = nullptr, *label = nullptr, *offsets = nullptr,
+             *indices = nullptr;
+    cudaEvent_t h2d_done = nullptr, labels_done = nullptr, compute_done = nullptr, d2h_done = nullptr;
+    bool used = false;
+};
+
 struct boba_ctx {
     int device = 0;
     uint64_t max_m = 0;
     uint32_t max_n = 0;
-    cudaStream_t stream = nullptr;
-    uint32_t *I = nullptr, *J = nullptr, *I2 = nullptr, *J2 = nullptr, *indices = nullptr;
-    uint32_t *first = nullptr, *order = nullptr, *label = nullptr, *offsets = nullptr;
+    cudaStream_t stream = nullptr;  // compute
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    boba_slot slot[2];
+    uint32_t *I2 = nullptr, *J2 = nullptr, *first = nullptr;
     void* ws = nullptr;
     size_t ws_bytes = 0;
+    uint64_t submitted = 0;
 };
 
 extern "C" {
@@ -241,18 +254,24 @@ int boba_ctx_create(uint64_t max_m, uint32_t max_n, boba_ctx** out) {
     c->max_m = max_m;
     c->max_n = max_n;
     cudaGetDevice(&c->device);
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     const size_t mb = max_m * 4 + 16, nb = (size_t)max_n * 4 + 16;
     c->ws_bytes = boba_reorder_to_csr_workspace_size(max_m, max_n, 0);
-    if (e == cudaSuccess) e = cudaMalloc(&c->I, mb);
-    if (e == cudaSuccess) e = cudaMalloc(&c->J, mb);
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking);
+    for (boba_slot& S : c->slot) {
+        if (e == cudaSuccess) e = cudaMalloc(&S.I, mb);
+        if (e == cudaSuccess) e = cudaMalloc(&S.J, mb);
+        if (e == cudaSuccess) e = cudaMalloc(&S.indices, mb);
+        if (e == cudaSuccess) e = cudaMalloc(&S.order, nb);
+        if (e == cudaSuccess) e = cudaMalloc(&S.label, nb);
+        if (e == cudaSuccess) e = cudaMalloc(&S.offsets, nb + 4);
+        for (cudaEvent_t* ev : {&S.h2d_done, &S.labels_done, &S.compute_done, &S.d2h_done})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&c->I2, mb);
     if (e == cudaSuccess) e = cudaMalloc(&c->J2, mb);
-    if (e == cudaSuccess) e = cudaMalloc(&c->indices, mb);
     if (e == cudaSuccess) e = cudaMalloc(&c->first, nb);
-    if (e == cudaSuccess) e = cudaMalloc(&c->order, nb);
-    if (e == cudaSuccess) e = cudaMalloc(&c->label, nb);
-    if (e == cudaSuccess) e = cudaMalloc(&c->offsets, nb + 4);
     if (e == cudaSuccess) e = cudaMalloc(&c->ws, c->ws_bytes);
     if (e != cudaSuccess) {
         boba_ctx_destroy(c);
@@ -264,36 +283,82 @@ int boba_ctx_create(uint64_t max_m, uint32_t max_n, boba_ctx** out) {
 
 void boba_ctx_destroy(boba_ctx* c) {
     if (!c) return;
-    for (void* p : {(void*)c->I, (void*)c->J, (void*)c->I2, (void*)c->J2, (void*)c->indices, (void*)c->first,
-                    (void*)c->order, (void*)c->label, (void*)c->offsets, c->ws})
+    for (cudaStream_t st : {c->stream, c->h2d, c->d2h})
+        if (st) cudaStreamSynchronize(st);
+    for (boba_slot& S : c->slot) {
+        for (void* p : {(void*)S.I, (void*)S.J, (void*)S.indices, (void*)S.order, (void*)S.label, (void*)S.offsets})
+            if (p) cudaFree(p);
+        for (cudaEvent_t ev : {S.h2d_done, S.labels_done, S.compute_done, S.d2h_done})
+            if (ev) cudaEventDestroy(ev);
+    }
+    for (void* p : {(void*)c->I2, (void*)c->J2, (void*)c->first, c->ws})
         if (p) cudaFree(p);
-    if (c->stream) cudaStreamDestroy(c->stream);
+    for (cudaStream_t st : {c->stream, c->h2d, c->d2h})
+        if (st) cudaStreamDestroy(st);
     delete c;
+}
+
+int boba_ctx_submit_host(boba_ctx* c, const uint32_t* I_h, const uint32_t* J_h, uint64_t m, uint32_t n,
+                         uint32_t* order_h, uint32_t* label_h, uint32_t* I2_h, uint32_t* J2_h, uint32_t* offsets_h,
+                         uint32_t* indices_h, uint64_t* ticket) {
+    REQUIRE(c, "boba_ctx_submit_host: NULL context");
+    REQUIRE(m <= c->max_m && n <= c->max_n, "boba_ctx_submit_host: graph exceeds the context capacity");
+    REQUIRE(order_h && label_h && offsets_h && (indices_h || m == 0) && ((I_h && J_h) || m == 0),
+            "boba_ctx_submit_host: NULL host buffer");
+    REQUIRE(n > 0, "boba_ctx_submit_host: n must be positive");
+    boba_slot& S = c->slot[c->submitted & 1];
+    cudaError_t e = cudaSuccess;
+    if (S.used) {
+        // the slot's previous graph: its compute must be done reading I, J before
+        // they are overwritten, and its D2H done before its outputs are
+        e = cudaStreamWaitEvent(c->h2d, S.compute_done, 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, S.d2h_done, 0);
+    }
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(S.I, I_h, m * 4, cudaMemcpyHostToDevice, c->h2d);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(S.J, J_h, m * 4, cudaMemcpyHostToDevice, c->h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(S.h2d_done, c->h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, S.h2d_done, 0);
+    if (e != cudaSuccess) return cuda_status(e, "boba_ctx_submit_host: H2D");
+    // labels_done is recorded after compaction: order and label go home while
+    // relabel and COO->CSR run
+    void* evs[5] = {nullptr, nullptr, S.labels_done, nullptr, S.compute_done};
+    if (int rc = boba_reorder_to_csr_timed(S.I, S.J, nullptr, m, n, c->first, S.order, S.label, c->I2, c->J2,
+                                           S.offsets, S.indices, nullptr, c->ws, c->ws_bytes, c->stream, evs))
+        return rc;
+    e = cudaStreamWaitEvent(c->d2h, S.labels_done, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(order_h, S.order, (size_t)n * 4, cudaMemcpyDeviceToHost, c->d2h);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(label_h, S.label, (size_t)n * 4, cudaMemcpyDeviceToHost, c->d2h);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->d2h, S.compute_done, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(offsets_h, S.offsets, ((size_t)n + 1) * 4, cudaMemcpyDeviceToHost, c->d2h);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(indices_h, S.indices, m * 4, cudaMemcpyDeviceToHost, c->d2h);
+    // I2/J2 are shared by both slots: their copies finish before the next compute starts
+    if (e == cudaSuccess && I2_h && m) e = cudaMemcpyAsync(I2_h, c->I2, m * 4, cudaMemcpyDeviceToHost, c->d2h);
+    if (e == cudaSuccess && J2_h && m) e = cudaMemcpyAsync(J2_h, c->J2, m * 4, cudaMemcpyDeviceToHost, c->d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(S.d2h_done, c->d2h);
+    if (e == cudaSuccess && (I2_h || J2_h)) e = cudaStreamWaitEvent(c->stream, S.d2h_done, 0);
+    if (e != cudaSuccess) return cuda_status(e, "boba_ctx_submit_host: D2H");
+    S.used = true;
+    if (ticket) *ticket = c->submitted;
+    c->submitted++;
+    return BOBA_OK;
+}
+
+int boba_ctx_wait(boba_ctx* c, uint64_t ticket) {
+    REQUIRE(c, "boba_ctx_wait: NULL context");
+    REQUIRE(ticket < c->submitted, "boba_ctx_wait: ticket %llu was never submitted", (unsigned long long)ticket);
+    // the slot's d2h_done event is the newest graph in that slot; graphs of a
+    // slot complete in submission order, so waiting on it covers `ticket`
+    return cuda_status(cudaEventSynchronize(c->slot[ticket & 1].d2h_done), "boba_ctx_wait");
 }
 
 int boba_ctx_reorder_to_csr_host(boba_ctx* c, const uint32_t* I_h, const uint32_t* J_h, uint64_t m, uint32_t n,
                                  uint32_t* order_h, uint32_t* label_h, uint32_t* I2_h, uint32_t* J2_h,
                                  uint32_t* offsets_h, uint32_t* indices_h) {
-    REQUIRE(c, "boba_ctx_reorder_to_csr_host: NULL context");
-    REQUIRE(m <= c->max_m && n <= c->max_n, "boba_ctx_reorder_to_csr_host: graph exceeds the context capacity");
-    REQUIRE(order_h && label_h && offsets_h && (indices_h || m == 0) && ((I_h && J_h) || m == 0),
-            "boba_ctx_reorder_to_csr_host: NULL host buffer");
-    cudaStream_t s = c->stream;
-    cudaError_t e = cudaSuccess;
-    if (m) e = cudaMemcpyAsync(c->I, I_h, m * 4, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && m) e = cudaMemcpyAsync(c->J, J_h, m * 4, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return cuda_status(e, "boba_ctx_reorder_to_csr_host: H2D");
-    if (int rc = boba_reorder_to_csr(c->I, c->J, nullptr, m, n, c->first, c->order, c->label, c->I2, c->J2,
-                                     c->offsets, c->indices, nullptr, c->ws, c->ws_bytes, s))
+    uint64_t t = 0;
+    if (n == 0) return BOBA_OK;
+    if (int rc = boba_ctx_submit_host(c, I_h, J_h, m, n, order_h, label_h, I2_h, J2_h, offsets_h, indices_h, &t))
         return rc;
-    e = cudaMemcpyAsync(order_h, c->order, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(label_h, c->label, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(offsets_h, c->offsets, ((size_t)n + 1) * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && m) e = cudaMemcpyAsync(indices_h, c->indices, m * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && I2_h && m) e = cudaMemcpyAsync(I2_h, c->I2, m * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && J2_h && m) e = cudaMemcpyAsync(J2_h, c->J2, m * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    return cuda_status(e, "boba_ctx_reorder_to_csr_host");
+    return boba_ctx_wait(c, t);
 }
 
 int boba_narrow_ids(const int64_t* in, uint64_t count, uint64_t bound, uint32_t* out, int64_t* bad_index,

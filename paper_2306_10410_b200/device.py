@@ -268,6 +268,21 @@ class HostPipeline:
         N.check(N.lib.boba_ctx_reorder_to_csr_host(self._ctx, ptr(I_host), ptr(J_host), m, n, ptr(order),
                                                    ptr(label), ptr(I2), ptr(J2), ptr(offsets), ptr(indices)))
 
+    def submit(self, I_host, J_host, n, order, label, offsets, indices, I2=None, J2=None) -> int:
+        """Asynchronous run: enqueues the graph and returns a ticket for wait().
+        Two graphs can be in flight; their copies overlap each other and the
+        compute.  Inputs must stay unchanged and outputs unread until wait()."""
+        ptr = lambda a: None if a is None else ctypes.c_void_p(  # noqa: E731
+            a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data)
+        m = I_host.numel() if isinstance(I_host, torch.Tensor) else I_host.size
+        t = ctypes.c_uint64()
+        N.check(N.lib.boba_ctx_submit_host(self._ctx, ptr(I_host), ptr(J_host), m, n, ptr(order), ptr(label),
+                                           ptr(I2), ptr(J2), ptr(offsets), ptr(indices), ctypes.byref(t)))
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        N.check(N.lib.boba_ctx_wait(self._ctx, ticket))
+
     def close(self):
         if self._ctx:
             N.lib.boba_ctx_destroy(self._ctx)

@@ -300,6 +300,33 @@ def test_host_pipeline_matches_device(dev):
     hp.close()
 
 
+def test_host_pipeline_async_graphs_in_flight(dev):
+    """boba_ctx_submit_host / boba_ctx_wait: five different graphs (different
+    sizes too) submitted back to back through the two buffer slots; each
+    graph's host outputs must equal the oracle's for that graph."""
+    import torch
+
+    graphs = []
+    for k, (scale, ef) in enumerate([(12, 8), (14, 16), (10, 4), (13, 8), (12, 16)]):
+        I, J = dev.generate_rmat(scale, ef, seed=10 + k)
+        graphs.append((1 << scale, I.cpu().numpy().view(np.uint32).copy(), J.cpu().numpy().view(np.uint32).copy()))
+    max_m = max(g[1].size for g in graphs)
+    hp = dev.HostPipeline(max_m, 1 << 14)
+    outs, tickets = [], []
+    for n, hI, hJ in graphs:
+        o = (np.empty(n, np.uint32), np.empty(n, np.uint32), np.empty(n + 1, np.uint32), np.empty(hI.size, np.uint32))
+        outs.append(o)
+        tickets.append(hp.submit(hI, hJ, n, *o))
+    for t in tickets:
+        hp.wait(t)
+    torch.cuda.synchronize()
+    for (n, hI, hJ), (order, label, off, idx) in zip(graphs, outs):
+        o_order, o_label, _, _, o_off, o_idx, _ = oracle.pipeline(hI.astype(np.int64), hJ.astype(np.int64), n)
+        assert np.array_equal(order, o_order) and np.array_equal(label, o_label)
+        assert np.array_equal(off, o_off) and np.array_equal(idx, o_idx)
+    hp.close()
+
+
 @pytest.mark.parametrize("scale,ef", [(12, 16), (20, 16)])
 def test_degree_orders_and_destination_sort_vs_oracle(bb, dev, scale, ef):
     """R-MAT (heavy ties in degree) through the C ABI vs the oracle."""
