@@ -23,6 +23,8 @@
 //    for 16-bit tags, a single sweep keeps a per-CTA set of vertices already
 //    finalised instead (insert-if-empty; CTA barrier per iteration keeps the
 //    invariant first[v] < lowest position still to come).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "hubs.cuh"
 #include "kernels.cuh"
@@ -151,6 +153,99 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* firs
     }
 }
 
+// Static-mode sweep, lean form: each of the two position ranges is walked
+// separately (uniform pointer and base, no per-quad range select), SeenSet
+// membership is a SWAR zero-lane test on the bucket's 64 bits, and the guard
+// load and the atomicMin are predicated instructions, not branches.
+template <int TW>
+__device__ __forceinline__ bool seen_swar(const unsigned long long* set, const HubHash& hh, uint32_t v) {
+    constexpr uint32_t kTagMask = (1u << TW) - 1u;
+    constexpr uint32_t kOnes = TW == 8 ? 0x01010101u : 0x00010001u;
+    constexpr uint32_t kHigh = kOnes << (TW - 1);
+    uint32_t b, tag;
+    hh.split(v, b, tag);
+    const uint2 w = reinterpret_cast<const uint2*>(set)[b];
+    const uint32_t rep = tag * kOnes;
+    const uint32_t x0 = w.x ^ rep, x1 = w.y ^ rep;  // a lane equal to tag -> a zero lane
+    const uint32_t z = (((x0 - kOnes) & ~x0) | ((x1 - kOnes) & ~x1)) & kHigh;
+    return z != 0 && tag != kTagMask;               // all-ones tags are never inserted (empty marker)
+}
+
+__device__ __forceinline__ uint32_t ld_cg_pred(const uint32_t* p, bool pred) {
+    uint32_t r = 0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cg.u32 %0, [%1];\n\t}"
+                 : "+r"(r)
+                 : "l"(p), "r"((uint32_t)pred));
+    return r;
+}
+__device__ __forceinline__ void red_min_pred(uint32_t* p, uint32_t v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.relaxed.gpu.global.min.u32 [%0], %1;\n\t}" ::"l"(p),
+                 "r"(v), "r"((uint32_t)pred)
+                 : "memory");
+}
+
+template <int TW>
+__device__ __forceinline__ void sweep_static(const uint4* __restrict__ src, uint64_t nq, uint32_t base,
+                                             uint32_t* first, const unsigned long long* set, const HubHash& hh) {
+    constexpr uint64_t kIter = (uint64_t)kFhNT * kFhQuads;
+    const uint64_t iters = ceil_div(nq, kIter);
+    for (uint64_t it = blockIdx.x; it < iters; it += gridDim.x) {
+        const uint64_t q0 = it * kIter + threadIdx.x;
+        uint4 q[kFhQuads];
+        bool ok[kFhQuads];
+#pragma unroll
+        for (int k = 0; k < kFhQuads; k++) {
+            const uint64_t w = q0 + (uint64_t)k * kFhNT;
+            ok[k] = w < nq;
+            q[k] = ok[k] ? __ldg(src + w) : make_uint4(0, 0, 0, 0);
+        }
+        bool need[kFhQuads][4];
+#pragma unroll
+        for (int k = 0; k < kFhQuads; k++) {
+            const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+            for (int j = 0; j < 4; j++) need[k][j] = ok[k] && !seen_swar<TW>(set, hh, vs[j]);
+        }
+        uint32_t cur[kFhQuads][4];
+#pragma unroll
+        for (int k = 0; k < kFhQuads; k++) {
+            const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+            for (int j = 0; j < 4; j++) cur[k][j] = ld_cg_pred(first + vs[j], need[k][j]);
+        }
+#pragma unroll
+        for (int k = 0; k < kFhQuads; k++) {
+            const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+            const uint32_t p0 = base + 4u * (uint32_t)(q0 + (uint64_t)k * kFhNT);
+#pragma unroll
+            for (int j = 0; j < 4; j++) red_min_pred(first + vs[j], p0 + j, need[k][j] && p0 + j < cur[k][j]);
+        }
+    }
+}
+
+template <int TW>
+__global__ void __launch_bounds__(kFhNT, 1) k_first_hit_static(Ranges r, uint32_t* first,
+                                                               const unsigned long long* __restrict__ seen_g,
+                                                               HubHash hh) {
+    extern __shared__ unsigned long long smem_u64[];
+    for (int i = threadIdx.x; i < kHubBuckets; i += kFhNT) smem_u64[i] = __ldg(seen_g + i);
+    __syncthreads();
+    sweep_static<TW>(reinterpret_cast<const uint4*>(r.a), r.qa, r.base_a, first, smem_u64, hh);
+    sweep_static<TW>(reinterpret_cast<const uint4*>(r.b), r.qb, r.base_b, first, smem_u64, hh);
+}
+
+template <int TW>
+static void launch_static(const Ranges& r, uint32_t* first, const unsigned long long* seen_g, const HubHash& hh,
+                          int num_sms, cudaStream_t s) {
+    const size_t smem = sizeof(unsigned long long) * kHubBuckets;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_first_hit_static<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_first_hit_static<TW><<<num_sms, kFhNT, smem, s>>>(r, first, seen_g, hh);
+}
+
 // SeenSet from the prefix: every vertex whose first occurrence is one of the
 // prefix positions gets its tag into a free 16-bit lane of its bucket.
 template <int TW>
@@ -235,6 +330,7 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
         const uint64_t quads = m >> 2;
         const uint32_t prefix = seen_prefix(hh.tag_bits);
         const bool two_stage = seen_ws && !relaxed && hh.tag_bits <= 16 && m >= 16ull * prefix;
+        static const bool lean = !getenv("BOBA_FH_OLD");
         if (two_stage) {
             unsigned long long* set = static_cast<unsigned long long*>(seen_ws);
             const uint64_t qp = prefix / 4;
@@ -245,10 +341,12 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
             Ranges r2{I + prefix, quads - qp, base_i + prefix, J, quads, base_j};
             if (hh.tag_bits <= 8) {
                 k_seen_build<8><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
-                launch_sweep<false, true, 8>(r2, first, set, hh, num_sms, s);
+                if (lean) launch_static<8>(r2, first, set, hh, num_sms, s);
+                else launch_sweep<false, true, 8>(r2, first, set, hh, num_sms, s);
             } else {
                 k_seen_build<16><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
-                launch_sweep<false, true, 16>(r2, first, set, hh, num_sms, s);
+                if (lean) launch_static<16>(r2, first, set, hh, num_sms, s);
+                else launch_sweep<false, true, 16>(r2, first, set, hh, num_sms, s);
             }
         } else {
             Ranges r{I, quads, base_i, J, quads, base_j};
