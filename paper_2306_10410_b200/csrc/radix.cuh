@@ -174,6 +174,13 @@ __device__ __forceinline__ void rank_slots(const uint32_t (&key)[IPT], uint32_t 
     }
 }
 
+// Staging slot of tile rank r.  Sorted or nearly sorted keys (a BOBA-ordered
+// grid) give every digit the same count, so a warp's 32 ranks are spaced by a
+// multiple of 16 entries -- 16 x 8 B = one full bank cycle -- and all land in
+// one bank pair; XOR-ing the low 4 bits with the next 4 spreads them (a
+// bijection on every aligned group of 256 slots).
+__device__ __forceinline__ uint32_t kv_swz(uint32_t r) { return r ^ ((r >> 4) & 15u); }
+
 template <int RB, int NT, int IPT, int MINB, typename Op>
 __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in, uint64_t m,
@@ -285,14 +292,14 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     for (int i = 0; i < IPT; i++) {
         if (rank[i] != 0xFFFFFFFFu) {
             const uint32_t r = rank[i] + wh[(i / (IPT / C::SUB)) * B + op(key[i])];
-            s_kv[r] = make_uint2(key[i], vals_in ? wraw[i * 32 + lane] : (uint32_t)(wslot + (uint64_t)i * 32 + lane));
+            s_kv[kv_swz(r)] = make_uint2(key[i], vals_in ? wraw[i * 32 + lane] : (uint32_t)(wslot + (uint64_t)i * 32 + lane));
         }
     }
     __syncthreads();
     const uint64_t rem = m - tile_base;
     const int items = rem < (uint64_t)TILE ? (int)rem : TILE;
     for (int j = threadIdx.x; j < items; j += NT) {
-        const uint2 kv = s_kv[j];
+        const uint2 kv = s_kv[kv_swz(j)];
         const uint32_t d = op(kv.x);
         const uint32_t g = s_glob[d] + (uint32_t)j;
         if (keys_out) keys_out[g] = kv.x;
@@ -305,7 +312,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
             // at 0xFFFFFFFF; empty rows are filled by a suffix-min afterwards.
             if (j == (int)s_off[d])
                 atomicMin(row_starts + kv.x, g);
-            else if (s_kv[j - 1].x != kv.x)
+            else if (s_kv[kv_swz(j - 1)].x != kv.x)
                 row_starts[kv.x] = g;
         }
     }
