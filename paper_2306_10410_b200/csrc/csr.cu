@@ -103,9 +103,13 @@ __global__ void k_row_starts(const uint32_t* __restrict__ keys, uint64_t m, uint
     if (blockIdx.x == 0 && threadIdx.x == 0) offsets[n] = (uint32_t)m;
 }
 
-constexpr int kSmNT = 256, kSmIPT = 8, kSmTile = kSmNT * kSmIPT;
+constexpr int kSmNT = 256, kSmIPT = 16, kSmTile = kSmNT * kSmIPT;
 
-// In-place suffix minimum over data[0..count): tiles are taken from the end.
+// In-place suffix minimum over data[0..count).  Tiles are aligned to
+// multiples of kSmTile from the bottom and taken from the top (tile k of T
+// covers [(T-1-k) kSmTile, ...)), so every thread's 16 elements are one
+// 64-byte aligned run read and written with 16-byte accesses; thread 0 owns
+// the topmost run.
 __global__ void __launch_bounds__(kSmNT) k_suffix_min(uint32_t* data, uint64_t count, unsigned long long* status,
                                                       unsigned* tile_counter) {
     __shared__ unsigned s_tile;
@@ -114,17 +118,23 @@ __global__ void __launch_bounds__(kSmNT) k_suffix_min(uint32_t* data, uint64_t c
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const uint64_t tile = s_tile;
-    const uint64_t hi = count - tile * kSmTile;               // exclusive end of this tile
-    const long long lo_t = (long long)hi - kSmTile;
-    // thread t owns elements [hi - (t+1)*IPT, hi - t*IPT), scanned from the top
+    const uint64_t T = ceil_div(count, kSmTile);
+    const uint64_t r0 = (T - 1 - tile) * kSmTile + (uint64_t)(kSmNT - 1 - threadIdx.x) * kSmIPT;  // run start
+    const bool vec = r0 + kSmIPT <= count && (reinterpret_cast<uintptr_t>(data) & 15) == 0;
     uint32_t v[kSmIPT];
+    if (vec) {
+#pragma unroll
+        for (int q = 0; q < kSmIPT / 4; q++) {
+            const uint4 x = reinterpret_cast<const uint4*>(data + r0)[q];
+            v[4 * q] = x.x, v[4 * q + 1] = x.y, v[4 * q + 2] = x.z, v[4 * q + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kSmIPT; k++) v[k] = r0 + k < count ? data[r0 + k] : 0xFFFFFFFFu;
+    }
     uint32_t run = 0xFFFFFFFFu;
 #pragma unroll
-    for (int k = 0; k < kSmIPT; k++) {
-        const long long i = (long long)hi - 1 - (long long)threadIdx.x * kSmIPT - k;
-        v[k] = (i >= 0 && i >= lo_t) ? data[i] : 0xFFFFFFFFu;
-        run = v[k] < run ? v[k] : run;
-    }
+    for (int k = 0; k < kSmIPT; k++) run = v[k] < run ? v[k] : run;
     // exclusive suffix-min across threads (thread 0 is the top of the tile)
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     uint32_t inc = run;
@@ -162,10 +172,18 @@ __global__ void __launch_bounds__(kSmNT) k_suffix_min(uint32_t* data, uint64_t c
     const unsigned long long c = s_carry;
     uint32_t acc = c < (unsigned long long)ex ? (uint32_t)c : ex;
 #pragma unroll
-    for (int k = 0; k < kSmIPT; k++) {
-        const long long i = (long long)hi - 1 - (long long)threadIdx.x * kSmIPT - k;
+    for (int k = kSmIPT - 1; k >= 0; k--) {  // top of the run first
         acc = v[k] < acc ? v[k] : acc;
-        if (i >= 0 && i >= lo_t) data[i] = acc;
+        v[k] = acc;
+    }
+    if (vec) {
+#pragma unroll
+        for (int q = 0; q < kSmIPT / 4; q++)
+            reinterpret_cast<uint4*>(data + r0)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kSmIPT; k++)
+            if (r0 + k < count) data[r0 + k] = v[k];
     }
 }
 

@@ -89,8 +89,10 @@ __global__ void __launch_bounds__(NT) k_radix_upsweep(const uint32_t* __restrict
 }
 
 // ------------------------------------------------- exclusive scan (u32) ---
-constexpr int kScanTileNT = 256, kScanTileIPT = 8, kScanTile = kScanTileNT * kScanTileIPT;
+constexpr int kScanTileNT = 256, kScanTileIPT = 16, kScanTile = kScanTileNT * kScanTileIPT;
 
+// Each thread owns 16 consecutive words (four 16-byte accesses when the run is
+// in bounds and data is 16-byte aligned).
 __global__ void __launch_bounds__(kScanTileNT) k_scan_u32(uint32_t* data, uint64_t count, uint32_t add,
                                                           unsigned long long* status, unsigned* tile_counter) {
     __shared__ unsigned s_tile;
@@ -100,13 +102,21 @@ __global__ void __launch_bounds__(kScanTileNT) k_scan_u32(uint32_t* data, uint64
     __syncthreads();
     const uint64_t tile = s_tile;
     const uint64_t i0 = tile * kScanTile + (uint64_t)threadIdx.x * kScanTileIPT;
+    const bool vec = i0 + kScanTileIPT <= count && (reinterpret_cast<uintptr_t>(data) & 15) == 0;
     uint32_t c[kScanTileIPT];
+    if (vec) {
+#pragma unroll
+        for (int q = 0; q < kScanTileIPT / 4; q++) {
+            const uint4 x = reinterpret_cast<const uint4*>(data + i0)[q];
+            c[4 * q] = x.x, c[4 * q + 1] = x.y, c[4 * q + 2] = x.z, c[4 * q + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanTileIPT; k++) c[k] = (i0 + k < count) ? data[i0 + k] : 0u;
+    }
     uint32_t sum = 0;
 #pragma unroll
-    for (int k = 0; k < kScanTileIPT; k++) {
-        c[k] = (i0 + k < count) ? data[i0 + k] : 0u;
-        sum += c[k];
-    }
+    for (int k = 0; k < kScanTileIPT; k++) sum += c[k];
     uint32_t total;
     uint32_t ex_t = block_exclusive_sum<kScanTileNT>(sum, s_scan, &total);
     if (threadIdx.x < 32) {
@@ -122,8 +132,18 @@ __global__ void __launch_bounds__(kScanTileNT) k_scan_u32(uint32_t* data, uint64
     uint32_t run = add + (uint32_t)s_excl + ex_t;
 #pragma unroll
     for (int k = 0; k < kScanTileIPT; k++) {
-        if (i0 + k < count) data[i0 + k] = run;
-        run += c[k];
+        const uint32_t x = c[k];
+        c[k] = run;
+        run += x;
+    }
+    if (vec) {
+#pragma unroll
+        for (int q = 0; q < kScanTileIPT / 4; q++)
+            reinterpret_cast<uint4*>(data + i0)[q] = make_uint4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanTileIPT; k++)
+            if (i0 + k < count) data[i0 + k] = c[k];
     }
 }
 
