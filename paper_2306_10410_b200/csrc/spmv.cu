@@ -28,6 +28,7 @@
 namespace boba {
 
 constexpr int kSpNT = 256, kSpIPT = 8, kSpTile = kSpNT * kSpIPT;
+constexpr int kSpShort = 8;  // longest in-tile row the per-row fold takes (longer: divergent folds)
 
 // Streaming loads that must not evict the x vector's hot lines from L1.
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
@@ -74,47 +75,58 @@ __global__ void k_spmv_partition(const uint32_t* __restrict__ offsets, uint32_t 
     coords[b] = (uint32_t)merge_search(offsets + 1, n, 0, m, d);
 }
 
-__device__ __forceinline__ void group_bar(int id) {
-    if (id == 0)
-        __syncthreads();
-    else
-        asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kSpNT) : "memory");
+// Merge-path search inside a tile, all tile-relative 32-bit: a[] holds the
+// row ends minus the tile's first nonzero index.
+__device__ __forceinline__ uint32_t merge_search_rel(const uint32_t* a, uint32_t a_len, uint32_t b_len, uint32_t diag) {
+    uint32_t lo = diag > b_len ? diag - b_len : 0, hi = diag < a_len ? diag : a_len;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] <= diag - mid - 1)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
 }
 
-// One merge-path tile processed by kSpNT threads (gt = thread index within
-// the group, bar = the group's barrier id).  Every row that ends inside the
-// tile is written here; the first row the tile ends may have started in
-// earlier tiles -- its partial sum is written and fixed up by k_spmv_carry (no
-// tile ever waits on another).  x entries below kx come from shared memory.
+// One merge-path tile (kSpTile merge items) processed by a CTA of kSpNT
+// threads.  Every row that ends inside the tile is written here; the first
+// row the tile ends may have started in earlier tiles -- its partial sum is
+// written and fixed up by k_spmv_carry (no tile ever waits on another).
+// Inside the tile all indices are 32-bit and relative to the tile's first
+// row (i0) and first nonzero (j0); only the global loads and stores use
+// 64-bit addresses.
 template <typename T>
-__device__ __forceinline__ void spmv_tile(uint64_t tile, int gt, int bar, const uint32_t* __restrict__ offsets,
+__device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restrict__ offsets,
                                           const uint32_t* __restrict__ indices, const T* __restrict__ w,
                                           const T* __restrict__ x, T* __restrict__ y, uint32_t n, uint64_t m,
                                           const uint32_t* __restrict__ coords, uint32_t* __restrict__ tile_head,
-                                          T* __restrict__ tile_tail, uint32_t* s_end, T* s_val, SegValT<T>* s_warp,
-                                          const T* s_x, uint32_t kx) {
+                                          T* __restrict__ tile_tail, uint32_t* s_end, T* s_val, SegValT<T>* s_warp) {
     using SegVal = SegValT<T>;
+    const uint32_t gt = threadIdx.x;
     const uint64_t total = (uint64_t)n + m;
     const uint64_t d0 = tile * kSpTile;
-    const uint64_t d1 = d0 + kSpTile < total ? d0 + kSpTile : total;
-    const uint64_t i0 = __ldg(coords + tile), i1 = __ldg(coords + tile + 1);
-    const uint64_t j0 = d0 - i0, j1 = d1 - i1;
-    const uint32_t nrows = (uint32_t)(i1 - i0), nnz = (uint32_t)(j1 - j0);
+    const uint32_t items_tile = (uint32_t)((d0 + kSpTile < total ? d0 + kSpTile : total) - d0);
+    const uint32_t i0 = __ldg(coords + tile), i1 = __ldg(coords + tile + 1);
+    const uint64_t j0 = d0 - i0;
+    const uint32_t nrows = i1 - i0, nnz = items_tile - nrows;
+    const uint32_t j0_32 = (uint32_t)j0;  // offsets are uint32: relative ends are exact mod 2^32
     for (uint32_t k = gt; k <= nrows; k += kSpNT)
-        s_end[k] = (i0 + k < n) ? ld_stream_u32(offsets + i0 + 1 + k) : 0xFFFFFFFFu;
+        s_end[k] = (i0 + k < n) ? ld_stream_u32(offsets + i0 + 1 + k) - j0_32 : 0xFFFFFFFFu;
     {
         // all index loads, then all x gathers in flight together (nnz <= kSpTile)
+        const uint32_t* ip = indices + j0;
         uint32_t col[kSpIPT];
 #pragma unroll
         for (int u = 0; u < kSpIPT; u++) {
             const uint32_t k = gt + u * kSpNT;
-            col[u] = k < nnz ? ld_stream_u32(indices + j0 + k) : 0u;
+            col[u] = k < nnz ? ld_stream_u32(ip + k) : 0u;
         }
         T p[kSpIPT];
 #pragma unroll
         for (int u = 0; u < kSpIPT; u++) {
             const uint32_t k = gt + u * kSpNT;
-            p[u] = k < nnz ? (col[u] < kx ? s_x[col[u]] : __ldg(x + col[u])) : T(0);
+            p[u] = k < nnz ? __ldg(x + col[u]) : T(0);
         }
 #pragma unroll
         for (int u = 0; u < kSpIPT; u++) {
@@ -122,34 +134,60 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, int gt, int bar, const 
             if (k < nnz) s_val[k] = w ? p[u] * __ldg(w + j0 + k) : p[u];
         }
     }
-    group_bar(bar);
+    // Short-row tiles (every row's in-tile part <= kSpShort nonzeros, e.g. a
+    // mesh): one thread folds each row straight from s_val -- no merge search,
+    // no segmented scan.  Tiles holding a longer row take the balanced
+    // merge-path fold below.  The choice depends on the matrix only, so y
+    // stays bitwise deterministic.
+    __syncthreads();
+    // (nnz > (nrows + 1) kSpShort: some row is long by pigeonhole -- skip the check)
+    if (nnz <= (nrows + 1) * (uint32_t)kSpShort) {
+        bool long_row = false;
+        for (uint32_t k = gt; k <= nrows; k += kSpNT) {
+            const uint32_t beg = k ? s_end[k - 1] : 0u, end = k < nrows ? s_end[k] : nnz;
+            long_row |= end - beg > (uint32_t)kSpShort;
+        }
+        if (!__syncthreads_or(long_row)) {
+            for (uint32_t k = gt; k < nrows; k += kSpNT) {
+                const uint32_t beg = k ? s_end[k - 1] : 0u, end = s_end[k];
+                T acc = 0;
+                for (uint32_t j = beg; j < end; j++) acc += s_val[j];
+                y[i0 + k] = acc;  // row 0 may have begun in earlier tiles: k_spmv_carry adds their tails
+            }
+            if (gt == 0) {
+                T tail = 0;
+                for (uint32_t j = nrows ? s_end[nrows - 1] : 0u; j < nnz; j++) tail += s_val[j];
+                tile_tail[tile] = tail;
+                tile_head[tile] = nrows ? i0 : 0xFFFFFFFFu;
+            }
+            return;
+        }
+    }
     // Per-thread sequential fold over kSpIPT merge items.
-    const uint32_t items_tile = (uint32_t)(d1 - d0);
     const uint32_t diag = gt * kSpIPT < items_tile ? gt * kSpIPT : items_tile;
-    uint32_t it = (uint32_t)merge_search(s_end, nrows, j0, nnz, diag);
+    uint32_t it = merge_search_rel(s_end, nrows, nnz, diag);
     uint32_t jt = diag - it;
     const uint32_t items = items_tile - diag < (uint32_t)kSpIPT ? items_tile - diag : (uint32_t)kSpIPT;
     T acc = 0, first_val = 0;
-    uint64_t first_row = 0;
+    uint32_t first_row = 0;
     bool emitted = false;
     for (uint32_t k = 0; k < items; k++) {
-        if (j0 + jt < (uint64_t)s_end[it]) {
+        if (jt < s_end[it]) {
             acc += s_val[jt];
             jt++;
         } else {
-            const uint64_t row = i0 + it;
             if (!emitted) {
-                first_row = row;
+                first_row = it;
                 first_val = acc;
                 emitted = true;
             } else {
-                y[row] = acc;
+                y[i0 + it] = acc;
             }
             acc = 0;
             it++;
         }
     }
-    // Segmented scan of (emitted, tail) over the group -> exclusive carry per thread.
+    // Segmented scan of (emitted, tail) over the CTA -> exclusive carry per thread.
     const unsigned lane = lane_id(), warp = gt >> 5;
     SegVal inc{emitted, acc};
 #pragma unroll
@@ -164,7 +202,7 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, int gt, int bar, const 
     lex.v = __shfl_up_sync(0xFFFFFFFFu, inc.v, 1);
     if (lane == 0) lex = SegVal{false, T(0)};
     if (lane == 31) s_warp[warp] = inc;
-    group_bar(bar);
+    __syncthreads();
     if (warp == 0) {
         SegVal wi = lane < kSpNT / 32 ? s_warp[lane] : SegVal{false, T(0)};
 #pragma unroll
@@ -185,15 +223,15 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, int gt, int bar, const 
             if (!wi.f) tile_head[tile] = 0xFFFFFFFFu;  // no row ends here
         }
     }
-    group_bar(bar);
+    __syncthreads();
     if (emitted) {
         const SegVal ex = seg_combine(s_warp[warp], lex);
-        y[first_row] = first_val + ex.v;
-        if (!ex.f) tile_head[tile] = (uint32_t)first_row;  // partial: earlier tiles add their tails
+        y[i0 + first_row] = first_val + ex.v;
+        if (!ex.f) tile_head[tile] = i0 + first_row;  // partial: earlier tiles add their tails
     }
 }
 
-// One tile per CTA (small problems, no x cache).
+// One merge-path tile per CTA.
 template <typename T>
 __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict__ offsets,
                                                       const uint32_t* __restrict__ indices,
@@ -206,8 +244,7 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
     __shared__ uint32_t s_end[kSpTile + 1];
     __shared__ T s_val[kSpTile];
     __shared__ SegValT<T> s_warp[kSpNT / 32];
-    spmv_tile<T>(blockIdx.x, threadIdx.x, 0, offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail, s_end,
-                 s_val, s_warp, nullptr, 0u);
+    spmv_tile<T>(blockIdx.x, offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail, s_end, s_val, s_warp);
 }
 
 // Chunk aggregates of the per-CTA (has_head, tail) pairs: a segmented sum
