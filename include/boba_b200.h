@@ -142,6 +142,20 @@ int boba_reorder_to_csr_timed(const uint32_t *I, const uint32_t *J, const double
                               double *weights_out, void *workspace, size_t workspace_bytes,
                               void *stream, void *const *events);
 
+/* --- Captured pipeline (CUDA graph) -------------------------------------
+ * Records one boba_reorder_to_csr call on these fixed device buffers (after
+ * one eager run, which also produces outputs) into a CUDA graph; each
+ * boba_graph_launch replays the whole pipeline with a single launch.  The
+ * buffers must stay allocated and the input contents may change between
+ * launches; (m, n) are fixed.  n >= 2. */
+typedef struct boba_graph boba_graph;
+int boba_reorder_to_csr_graph_create(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n,
+                                     uint32_t *first, uint32_t *order, uint32_t *label, uint32_t *I2,
+                                     uint32_t *J2, uint32_t *offsets, uint32_t *indices, void *workspace,
+                                     size_t workspace_bytes, boba_graph **out);
+int boba_graph_launch(boba_graph *graph, void *stream);
+void boba_reorder_to_csr_graph_destroy(boba_graph *graph);
+
 /* --- Host-buffer pipeline (end to end) ----------------------------------
  * A context owns device buffers for graphs up to (max_m, max_n) on the
  * current device plus a stream.  boba_ctx_reorder_to_csr_host copies I, J

@@ -59,6 +59,10 @@ SIGNATURES = {
     "boba_ctx_reorder_to_csr_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P], _I),
     "boba_ctx_submit_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_U64)], _I),
     "boba_ctx_wait": ([_P, _U64], _I),
+    "boba_reorder_to_csr_graph_create": ([_P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ,
+                                          ctypes.POINTER(_P)], _I),
+    "boba_graph_launch": ([_P, _P], _I),
+    "boba_reorder_to_csr_graph_destroy": ([_P], None),
     "boba_narrow_ids": ([_P, _U64, _U64, _P, ctypes.POINTER(ctypes.c_int64), _P], _I),
     "boba_widen_ids": ([_P, _U64, _P, _P], _I),
     "boba_exclusive_scan_workspace_size": ([_U64], _SZ),

@@ -59,6 +59,14 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 }  // namespace
 
+// Captured pipelines: one fused reorder->CSR call on fixed buffers recorded
+// into a CUDA graph, so a repeated step costs one graph launch instead of
+// ~21 kernel launches and their gaps.
+struct boba_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
 // Host-buffer contexts: two buffer slots so that consecutive graphs overlap
 // (H2D of graph k+1 and D2H of graph k run on their own copy streams while
 // the compute stream works); the compute-internal arrays (first, I2, J2,
@@ -245,6 +253,48 @@ int boba_reorder_to_csr(const uint32_t* I, const uint32_t* J, const double* w, u
                         void* stream) {
     return boba_reorder_to_csr_timed(I, J, w, m, n, first, order, label, I2, J2, offsets, indices, w_out, ws,
                                      ws_bytes, stream, nullptr);
+}
+
+int boba_reorder_to_csr_graph_create(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
+                                     uint32_t* order, uint32_t* label, uint32_t* I2, uint32_t* J2, uint32_t* offsets,
+                                     uint32_t* indices, void* ws, size_t ws_bytes, boba_graph** out) {
+    REQUIRE(out, "boba_reorder_to_csr_graph_create: out is NULL");
+    REQUIRE(n >= 2, "boba_reorder_to_csr_graph_create: n must be >= 2 (use boba_reorder_to_csr)");
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr_graph_create: stream");
+    // one eager run first: one-time kernel attribute setup happens outside the capture
+    int rc = boba_reorder_to_csr(I, J, nullptr, m, n, first, order, label, I2, J2, offsets, indices, nullptr, ws,
+                                 ws_bytes, st);
+    if (rc == BOBA_OK) e = cudaStreamSynchronize(st);
+    boba_graph* g = new boba_graph();
+    if (rc == BOBA_OK && e == cudaSuccess) e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (rc == BOBA_OK && e == cudaSuccess) {
+        rc = boba_reorder_to_csr(I, J, nullptr, m, n, first, order, label, I2, J2, offsets, indices, nullptr, ws,
+                                 ws_bytes, st);
+        cudaError_t e2 = cudaStreamEndCapture(st, &g->graph);
+        if (e == cudaSuccess) e = e2;
+    }
+    if (rc == BOBA_OK && e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    cudaStreamDestroy(st);
+    if (rc != BOBA_OK || e != cudaSuccess) {
+        boba_reorder_to_csr_graph_destroy(g);
+        return rc != BOBA_OK ? rc : cuda_status(e, "boba_reorder_to_csr_graph_create: capture");
+    }
+    *out = g;
+    return BOBA_OK;
+}
+
+int boba_graph_launch(boba_graph* g, void* stream) {
+    REQUIRE(g && g->exec, "boba_graph_launch: NULL graph");
+    return cuda_status(cudaGraphLaunch(g->exec, S(stream)), "boba_graph_launch");
+}
+
+void boba_reorder_to_csr_graph_destroy(boba_graph* g) {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
 }
 
 int boba_ctx_create(uint64_t max_m, uint32_t max_n, boba_ctx** out) {

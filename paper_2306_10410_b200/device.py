@@ -215,6 +215,35 @@ class Pipeline:
         return self
 
 
+class CapturedPipeline:
+    """A Pipeline's fused call on fixed inputs (I, J) captured into a CUDA
+    graph (boba_reorder_to_csr_graph_create); launch() replays the whole
+    step with one graph launch.  Creating it runs the pipeline once."""
+
+    def __init__(self, pipe: "Pipeline", I: torch.Tensor, J: torch.Tensor):
+        self.pipe, self.I, self.J = pipe, I, J  # keep the buffers alive
+        self._g = ctypes.c_void_p()
+        p = pipe
+        N.check(N.lib.boba_reorder_to_csr_graph_create(
+            _p(I), _p(J), I.numel(), p.n, _p(p.first), _p(p.order), _p(p.label), _p(p.I2), _p(p.J2), _p(p.offsets),
+            _p(p.indices), _p(p.ws), p.ws.numel(), ctypes.byref(self._g)))
+
+    def launch(self):
+        N.check(N.lib.boba_graph_launch(self._g, _s()))
+        return self.pipe
+
+    def close(self):
+        if self._g:
+            N.lib.boba_reorder_to_csr_graph_destroy(self._g)
+            self._g = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def generate_rmat(scale: int, edge_factor: int, seed: int, device=None):
     """Graph500 R-MAT edges (uint32) on the device; see oracle.rmat_edges."""
     dev = device or require_cuda()
