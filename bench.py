@@ -645,8 +645,7 @@ def run_sharded(args):
 
 def csr_passes(n):
     bits = 0 if n <= 1 else (n - 1).bit_length()
-    maxb = 11 if os.environ.get("BOBA_RADIX_CFG", "a").startswith("1") else 8
-    return 0 if bits == 0 else -(-bits // maxb)
+    return 0 if bits == 0 else -(-bits // 8)
 
 
 def launches_per_step(m, n):

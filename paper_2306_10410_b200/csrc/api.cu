@@ -228,19 +228,10 @@ int boba_reorder_to_csr_timed(const uint32_t* I, const uint32_t* J, const double
     e = boba::launch_compact(first, m, n, order, label, nullptr, hubs, rest, rest_bytes, sms, s);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: compact");
     mark(2);
-    // Optionally (BOBA_FUSE_H1=1) relabel also writes the first radix pass's tile
-    // histogram.  Off by default: measured at c2, the per-tile barrier in the
-    // latency-bound relabel (+80 us) costs more than the upsweep it saves (64 us).
-    int dbits = 0;
-    static const bool want_fuse = getenv("BOBA_FUSE_H1") != nullptr;
-    uint32_t* H1 = want_fuse ? boba::csr_first_pass_hist(rest, m, n, &dbits) : nullptr;
-    const bool fuse_h1 = H1 && (m & 3) == 0 &&
-                         ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(J) |
-                           reinterpret_cast<uintptr_t>(I2) | reinterpret_cast<uintptr_t>(J2)) & 15) == 0;
-    e = boba::launch_relabel(I, J, m, label, hubs, I2, J2, nullptr, n, sms, s, fuse_h1 ? H1 : nullptr, dbits);
+    e = boba::launch_relabel(I, J, m, label, hubs, I2, J2, nullptr, n, sms, s);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: relabel");
     mark(3);
-    e = boba::launch_coo_to_csr(I2, J2, w, m, n, nullptr, offsets, indices, w_out, rest, rest_bytes, sms, s, fuse_h1);
+    e = boba::launch_coo_to_csr(I2, J2, w, m, n, nullptr, offsets, indices, w_out, rest, rest_bytes, sms, s);
     (void)counts;
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: coo_to_csr");
     mark(4);

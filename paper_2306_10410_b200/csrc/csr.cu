@@ -205,31 +205,18 @@ __global__ void k_gather_payload(const uint32_t* __restrict__ eidx, uint64_t m, 
 
 // ----------------------------------------------------------------- host ---
 namespace {
-// Radix pass variants: (digit bits, threads, items per thread, min CTAs/SM).
-enum class Variant { R8x256, R8x512, R11x256 };
-
-Variant variant() {
-    const char* e = getenv("BOBA_RADIX_CFG");
-    if (e && e[0] == '1') return Variant::R11x256;
-    if (e && e[0] == 'b') return Variant::R8x512;
-
-    return Variant::R8x256;
-}
-int variant_bits(Variant v) { return v == Variant::R11x256 ? 11 : 8; }
-uint64_t variant_tile(Variant v) {
-    switch (v) {
-        case Variant::R8x256: return RadixCfg<8, 256, 16>::TILE;
-        case Variant::R8x512: return RadixCfg<8, 512, 16>::TILE;
-
-        default: return RadixCfg<11, 256, 16>::TILE;
-    }
-}
+// Radix passes: 8-bit digits (7- and <=6-bit passes use narrower
+// instantiations), 256 threads x 16 items = 4096-item tiles, 4 CTAs/SM.
+// Measured slower and removed: 11-bit digits (the tiles x 2048 histogram
+// outgrows the scan), 512x8 / 512x16 / 256x8 tiles, a persistent TMA
+// double-buffered downsweep, a onesweep (decoupled lookback) variant.
+constexpr int kRadixBits = 8;
+constexpr uint64_t kRadixTile = RadixCfg<8, 256, 16>::TILE;
 
 struct CsrPlan {
     int passes = 0;
     int shift[4] = {0, 0, 0, 0};
     int bits[4] = {0, 0, 0, 0};
-    Variant v = Variant::R8x512;
     uint64_t tile = 0;
 };
 
@@ -237,9 +224,7 @@ CsrPlan plan_for(uint32_t n) {
     CsrPlan p;
     const int kbits = n <= 1 ? 0 : 32 - __builtin_clz(n - 1);
     if (kbits == 0) return p;
-    p.v = variant();
-    const int maxb = variant_bits(p.v);
-    p.passes = (kbits + maxb - 1) / maxb;
+    p.passes = (kbits + kRadixBits - 1) / kRadixBits;
     int sh = 0;
     for (int i = 0; i < p.passes; i++) {
         const int b = kbits / p.passes + (i < kbits % p.passes ? 1 : 0);
@@ -247,7 +232,7 @@ CsrPlan plan_for(uint32_t n) {
         p.bits[i] = b;
         sh += b;
     }
-    p.tile = variant_tile(p.v);
+    p.tile = kRadixTile;
     return p;
 }
 
@@ -287,7 +272,7 @@ CsrWs carve(void* base, uint64_t m, uint32_t n) {
 template <int RB, int NT, int IPT, int MINB, typename Op = DigitShift>
 cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, Op op, int bits, uint32_t* H,
                           unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                          int num_sms, cudaStream_t s, uint32_t* row_starts = nullptr, bool skip_up = false) {
+                          int num_sms, cudaStream_t s, uint32_t* row_starts = nullptr) {
     using C = RadixCfg<RB, NT, IPT>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -299,7 +284,7 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
     const uint64_t tiles = ceil_div(m, C::TILE);
     const uint64_t hcount = tiles << bits;
     const uint64_t up_grid = tiles < (uint64_t)num_sms * 8 ? tiles : (uint64_t)num_sms * 8;
-    if (!skip_up) k_radix_upsweep<RB, NT, IPT, Op><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, op, bits, tiles, H);
+    k_radix_upsweep<RB, NT, IPT, Op><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, op, bits, tiles, H);
     cudaError_t e = cudaMemsetAsync(scan_status, 0, (ceil_div(hcount, kScanTile) + 1) * 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 4, s);
     if (e != cudaSuccess) return e;
@@ -314,44 +299,22 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
 template <int RB, int NT, int IPT, int MINB>
 cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits, uint32_t* H,
                        unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                       int num_sms, cudaStream_t s, uint32_t* row_starts, bool skip_up) {
+                       int num_sms, cudaStream_t s, uint32_t* row_starts) {
     const DigitShift op{shift, (1u << bits) - 1u};
     if (RB == 8 && bits <= 6)
         return radix_pass_op<6, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                           num_sms, s, row_starts, skip_up);
+                                                           num_sms, s, row_starts);
     if (RB == 8 && bits == 7)
         return radix_pass_op<7, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                           num_sms, s, row_starts, skip_up);
+                                                           num_sms, s, row_starts);
     return radix_pass_op<RB, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                        num_sms, s, row_starts, skip_up);
+                                                        num_sms, s, row_starts);
 }
 
-cudaError_t dispatch_pass(Variant v, const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits,
-                          uint32_t* H, unsigned long long* st, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                          int sms, cudaStream_t s, uint32_t* row_starts, bool skip_up) {
-    switch (v) {
-        case Variant::R8x256:
-            return radix_pass<8, 256, 16, 4>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s, row_starts,
-                                             skip_up);
-        case Variant::R8x512:
-            return radix_pass<8, 512, 16, 2>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s, row_starts,
-                                             skip_up);
-
-        default:
-            return radix_pass<11, 256, 16, 2>(kin, vin, m, shift, bits, H, st, counter, kout, vout, sms, s,
-                                              row_starts, skip_up);
-    }
-}
 }  // namespace
 
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool /*weighted*/) { return carve(nullptr, m, n).total; }
 
-uint32_t* csr_first_pass_hist(void* ws, uint64_t m, uint32_t n, int* dbits) {
-    const CsrPlan p = plan_for(n);
-    if (p.passes == 0 || p.tile != 4096 || m == 0) return nullptr;
-    *dbits = p.bits[0];
-    return carve(ws, m, n).H;
-}
 
 __global__ void k_iota(uint32_t* out, uint64_t count) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -421,7 +384,7 @@ cudaError_t launch_sort_pairs(const uint32_t* keys, const uint32_t* vals, uint64
         uint32_t* kout = last ? keys_out : W.bufs[(i & 1) * 2];
         uint32_t* vout = last ? vals_out : W.bufs[(i & 1) * 2 + 1];
         cudaError_t e = radix_pass<8, 256, 16, 4>(kin, vin, count, sh, bits, W.H, W.st, W.counter, kout, vout,
-                                                  num_sms, s, nullptr, false);
+                                                  num_sms, s, nullptr);
         if (e != cudaSuccess) return e;
         kin = kout;
         vin = vout;
@@ -495,7 +458,7 @@ cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* cou
 
 cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
                               const uint32_t* counts_in, uint32_t* offsets, uint32_t* indices, double* w_out,
-                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool h1_ready) {
+                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s) {
     const bool weighted = w != nullptr;
     CsrWs W = carve(ws, m, n);
     if (ws_bytes < W.total) return cudaErrorInvalidValue;
@@ -532,8 +495,8 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
         // pass i writes bufs[2(i&1)], bufs[2(i&1)+1]; it reads the other parity.
         uint32_t* kout = last ? nullptr : W.bufs[(i & 1) * 2];
         uint32_t* vout = (last && !weighted) ? indices : W.bufs[(i & 1) * 2 + 1];
-        e = dispatch_pass(p.v, kin, vin, m, p.shift[i], p.bits[i], W.H, W.scan_status, W.counters, kout, vout,
-                          num_sms, s, (last && !counts_in) ? offsets : nullptr, i == 0 && h1_ready);
+        e = radix_pass<8, 256, 16, 4>(kin, vin, m, p.shift[i], p.bits[i], W.H, W.scan_status, W.counters, kout, vout,
+                                      num_sms, s, (last && !counts_in) ? offsets : nullptr);
         if (e != cudaSuccess) return e;
         kin = kout;
         vin = vout;

@@ -23,8 +23,6 @@
 //    for 16-bit tags, a single sweep keeps a per-CTA set of vertices already
 //    finalised instead (insert-if-empty; CTA barrier per iteration keeps the
 //    invariant first[v] < lowest position still to come).
-#include <cstdlib>
-
 #include "common.cuh"
 #include "hubs.cuh"
 #include "kernels.cuh"
@@ -69,38 +67,17 @@ __device__ __forceinline__ void hit_dyn(uint32_t* first, uint32_t* set, uint32_t
     }
 }
 
-// Static mode: the SeenSet of vertices first seen in the prefix.
-template <int TW>  // tag width: 8 (8 lanes per bucket) or 16 (4 lanes)
-__device__ __forceinline__ bool seen(const unsigned long long* set, const HubHash& hh, uint32_t v) {
-    constexpr uint32_t kTagMask = (1u << TW) - 1u;
-    uint32_t b, tag;
-    hh.split(v, b, tag);
-    if (tag == kTagMask) return false;             // never inserted (all-ones marks an empty lane)
-    const uint2 w = reinterpret_cast<const uint2*>(set)[b];
-    if (TW == 8) {
-        const uint32_t rep = tag * 0x01010101u;
-        return (__vcmpeq4(w.x, rep) | __vcmpeq4(w.y, rep)) != 0;
-    } else {
-        const uint32_t rep = tag * 0x00010001u;
-        return (__vcmpeq2(w.x, rep) | __vcmpeq2(w.y, rep)) != 0;
-    }
-}
-
-template <bool RELAXED, bool STATIC, int TW = 16>
-__global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* first,
-                                                        const unsigned long long* __restrict__ seen_g, HubHash hh) {
+// Dynamic-mode sweep over I||J in position order (block-cyclic 16K-position
+// iterations, a CTA barrier per iteration keeps the set invariant).
+template <bool RELAXED>
+__global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* first) {
     extern __shared__ unsigned long long smem_u64[];
     uint32_t* set = reinterpret_cast<uint32_t*>(smem_u64);
-    if (STATIC) {
-        for (int i = threadIdx.x; i < kHubBuckets; i += kFhNT) smem_u64[i] = __ldg(seen_g + i);
-    } else {
-        for (int i = threadIdx.x; i < (1 << kFhSlotsLog2); i += kFhNT) set[i] = kEmpty;
-    }
+    for (int i = threadIdx.x; i < (1 << kFhSlotsLog2); i += kFhNT) set[i] = kEmpty;
     const uint64_t total_q = r.qa + r.qb;
     const uint64_t iters = ceil_div(total_q, (uint64_t)kFhNT * kFhQuads);
-    if (STATIC) __syncthreads();
     for (uint64_t it = blockIdx.x; it < iters; it += gridDim.x) {
-        if (!STATIC) __syncthreads();  // every warp has left the previous iteration
+        __syncthreads();  // every warp has left the previous iteration
         const uint64_t q0 = it * kFhNT * kFhQuads;
         const uint32_t iter_lo = (uint32_t)(q0 < r.qa ? r.base_a + 4 * q0 : r.base_b + 4 * (q0 - r.qa));
         uint4 q[kFhQuads];
@@ -117,43 +94,18 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* firs
                 pos[k] = (uint32_t)(4 * qi) + (inB ? r.base_b : r.base_a);
             }
         }
-        if (STATIC) {
-            // all set probes first, then all guard loads in flight together, then the atomics
-            bool need[kFhQuads][4];
-            uint32_t cur[kFhQuads][4];
 #pragma unroll
-            for (int k = 0; k < kFhQuads; k++) {
-                const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
-#pragma unroll
-                for (int j = 0; j < 4; j++) need[k][j] = ok[k] && !seen<TW>(smem_u64, hh, vs[j]);
-            }
-#pragma unroll
-            for (int k = 0; k < kFhQuads; k++) {
-                const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
-#pragma unroll
-                for (int j = 0; j < 4; j++) cur[k][j] = need[k][j] ? __ldcg(first + vs[j]) : 0u;
-            }
-#pragma unroll
-            for (int k = 0; k < kFhQuads; k++) {
-                const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
-#pragma unroll
-                for (int j = 0; j < 4; j++)
-                    if (need[k][j] && pos[k] + j < cur[k][j]) update<RELAXED>(first, vs[j], pos[k] + j, cur[k][j]);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < kFhQuads; k++) {
-                if (!ok[k]) continue;
-                hit_dyn<RELAXED>(first, set, q[k].x, pos[k], iter_lo);
-                hit_dyn<RELAXED>(first, set, q[k].y, pos[k] + 1, iter_lo);
-                hit_dyn<RELAXED>(first, set, q[k].z, pos[k] + 2, iter_lo);
-                hit_dyn<RELAXED>(first, set, q[k].w, pos[k] + 3, iter_lo);
-            }
+        for (int k = 0; k < kFhQuads; k++) {
+            if (!ok[k]) continue;
+            hit_dyn<RELAXED>(first, set, q[k].x, pos[k], iter_lo);
+            hit_dyn<RELAXED>(first, set, q[k].y, pos[k] + 1, iter_lo);
+            hit_dyn<RELAXED>(first, set, q[k].z, pos[k] + 2, iter_lo);
+            hit_dyn<RELAXED>(first, set, q[k].w, pos[k] + 3, iter_lo);
         }
     }
 }
 
-// Static-mode sweep, lean form: each of the two position ranges is walked
+// Static-mode sweep (stage 2 of the two-stage sweep): each of the two position ranges is walked
 // separately (uniform pointer and base, no per-quad range select), SeenSet
 // membership is a SWAR zero-lane test on the bucket's 64 bits, and the guard
 // load and the atomicMin are predicated instructions, not branches.
@@ -291,20 +243,18 @@ __global__ void k_first_hit_scalar(const uint32_t* __restrict__ I, const uint32_
     }
 }
 
-template <bool RELAXED, bool STATIC, int TW = 16>
-static void launch_sweep(const Ranges& r, uint32_t* first, const unsigned long long* seen_g, const HubHash& hh,
-                         int num_sms, cudaStream_t s) {
-    const size_t smem = STATIC ? sizeof(unsigned long long) * kHubBuckets : (sizeof(uint32_t) << kFhSlotsLog2);
+template <bool RELAXED>
+static void launch_sweep(const Ranges& r, uint32_t* first, int num_sms, cudaStream_t s) {
+    const size_t smem = sizeof(uint32_t) << kFhSlotsLog2;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_first_hit<RELAXED, STATIC, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(k_first_hit<RELAXED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     const uint64_t iters = ceil_div(r.qa + r.qb, (uint64_t)kFhNT * kFhQuads);
     if (iters == 0) return;
     const int grid = (int)(iters < (uint64_t)num_sms ? iters : (uint64_t)num_sms);
-    k_first_hit<RELAXED, STATIC, TW><<<grid, kFhNT, smem, s>>>(r, first, seen_g, hh);
+    k_first_hit<RELAXED><<<grid, kFhNT, smem, s>>>(r, first);
 }
 
 cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
@@ -330,30 +280,27 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
         const uint64_t quads = m >> 2;
         const uint32_t prefix = seen_prefix(hh.tag_bits);
         const bool two_stage = seen_ws && !relaxed && hh.tag_bits <= 16 && m >= 16ull * prefix;
-        static const bool lean = !getenv("BOBA_FH_OLD");
         if (two_stage) {
             unsigned long long* set = static_cast<unsigned long long*>(seen_ws);
             const uint64_t qp = prefix / 4;
             Ranges r1{I, qp, base_i, J, 0, base_j};
-            launch_sweep<false, false>(r1, first, nullptr, hh, num_sms, s);
+            launch_sweep<false>(r1, first, num_sms, s);
             err = cudaMemsetAsync(set, 0xFF, kHubTableBytes, s);
             if (err != cudaSuccess) return err;
             Ranges r2{I + prefix, quads - qp, base_i + prefix, J, quads, base_j};
             if (hh.tag_bits <= 8) {
                 k_seen_build<8><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
-                if (lean) launch_static<8>(r2, first, set, hh, num_sms, s);
-                else launch_sweep<false, true, 8>(r2, first, set, hh, num_sms, s);
+                launch_static<8>(r2, first, set, hh, num_sms, s);
             } else {
                 k_seen_build<16><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
-                if (lean) launch_static<16>(r2, first, set, hh, num_sms, s);
-                else launch_sweep<false, true, 16>(r2, first, set, hh, num_sms, s);
+                launch_static<16>(r2, first, set, hh, num_sms, s);
             }
         } else {
             Ranges r{I, quads, base_i, J, quads, base_j};
             if (relaxed)
-                launch_sweep<true, false>(r, first, nullptr, hh, num_sms, s);
+                launch_sweep<true>(r, first, num_sms, s);
             else
-                launch_sweep<false, false>(r, first, nullptr, hh, num_sms, s);
+                launch_sweep<false>(r, first, num_sms, s);
         }
         done = m & ~3ull;
     }

@@ -22,25 +22,18 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
                            uint32_t* n_seen_out, unsigned long long* hubs, void* ws, size_t ws_bytes, int num_sms,
                            cudaStream_t s);
 
-// H (may be NULL): also write the first radix pass's tile digit histogram
-// (csr_first_pass_hist), dbits = that pass's digit width; needs m % 4 == 0,
-// 16-byte aligned arrays and counts == NULL (else cudaErrorInvalidValue).
+// counts (may be NULL): also the out-degree histogram of the new rows
 cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,
                            const unsigned long long* hubs, uint32_t* I2, uint32_t* J2, uint32_t* counts, uint32_t n,
-                           int num_sms, cudaStream_t s, uint32_t* H = nullptr, int dbits = 0);
+                           int num_sms, cudaStream_t s);
 
 cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* counts, int num_sms, cudaStream_t s);
 cudaError_t launch_row_offsets(const uint32_t* counts, uint32_t n, uint32_t* offsets, unsigned long long* status,
                                unsigned* counter, cudaStream_t s);
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool weighted);
-// Where COO->CSR (with workspace ws) expects its first pass's tile histogram,
-// and that pass's digit bits; NULL if the plan has no radix pass or the tile
-// size differs from the relabel kernel's 4096 edges.
-uint32_t* csr_first_pass_hist(void* ws, uint64_t m, uint32_t n, int* dbits);
-// h1_ready: the first pass's tile histogram is already in place (relabel wrote it)
 cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
                               const uint32_t* counts_in, uint32_t* offsets, uint32_t* indices, double* w_out,
-                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool h1_ready = false);
+                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s);
 
 size_t spmv_workspace_bytes(uint32_t n, uint64_t m);
 cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,

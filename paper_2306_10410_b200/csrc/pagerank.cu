@@ -222,7 +222,7 @@ cudaError_t launch_pagerank(const uint32_t* offsets, const uint32_t* indices, co
         k_share<<<grid_of(m, num_sms), 256, 0, s>>>(W.src, w, W.ow, m, W.share);
     }
     e = launch_coo_to_csr(indices, W.src, W.share, m, n, nullptr, W.rev_off, W.rev_idx, W.rev_w, W.csr_ws,
-                          W.csr_bytes, num_sms, s, false);
+                          W.csr_bytes, num_sms, s);
     if (e != cudaSuccess) return e;
     // x0 = 1/n and the first dangling mass (kernels.py:97-101)
     const int G = pr_grid(n, num_sms);

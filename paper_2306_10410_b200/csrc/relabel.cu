@@ -27,18 +27,18 @@ constexpr int kRlNT = 1024;
 constexpr int kHubHistRows = 8192;
 
 // MODE: 0 relabel only; 1 + out-degree histogram of the new rows (counts, the
-// np.bincount of graph.py:270); 2 + the first radix pass's per-tile digit
-// histogram (H[d * tiles + t], tile = 4096 edges = one CTA iteration), so
-// COO->CSR can skip that pass's upsweep over I2.
+// np.bincount of graph.py:270).  (Also writing the first radix pass's tile
+// histogram here was measured: the per-tile barrier it needs costs more in
+// this latency-bound loop than the upsweep it saves.)
 template <int MODE, bool HUBS>
 __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ I, const uint4* __restrict__ J,
                                                       uint64_t quads, const uint32_t* __restrict__ label,
                                                       const unsigned long long* __restrict__ hubs, HubHash hh,
                                                       uint32_t n, uint4* __restrict__ I2, uint4* __restrict__ J2,
-                                                      uint32_t* counts, uint32_t* H, uint32_t dmask, uint64_t tiles) {
+                                                      uint32_t* counts) {
     extern __shared__ uint32_t sm32[];
     uint32_t* s_tab = sm32;                                                       // kHubWays x kHubBuckets
-    uint32_t* s_hist = sm32 + (HUBS ? kHubWays * kHubBuckets : 0);                // kHubHistRows or 256
+    uint32_t* s_hist = sm32 + (HUBS ? kHubWays * kHubBuckets : 0);                // kHubHistRows
     if (HUBS) {
         const uint4* src = reinterpret_cast<const uint4*>(hubs);
         for (int i = threadIdx.x; i < kHubWays * kHubBuckets / 4; i += kRlNT)
@@ -71,17 +71,7 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ 
         else
             atomicAdd(counts + r, 1u);
     };
-    // One CTA iteration = one 4096-edge tile (kRlNT quads).  MODE 2 double-buffers
-    // the tile histogram so each iteration needs a single barrier: a buffer is
-    // filled in iteration t, flushed (and re-zeroed) right after that barrier,
-    // and refilled only in t + 2, after the next barrier.
-    if (MODE == 2) {
-        for (int i = threadIdx.x; i < 512; i += kRlNT) s_hist[i] = 0;
-        __syncthreads();
-    }
-    int par = 0;
-    for (uint64_t t = blockIdx.x; t * kRlNT < quads; t += gridDim.x, par ^= 1) {
-        uint32_t* hb = s_hist + 256 * par;
+    for (uint64_t t = blockIdx.x; t * kRlNT < quads; t += gridDim.x) {
         const uint64_t q = t * kRlNT + threadIdx.x;
         if (q < quads) {
             const uint4 a = __ldg(I + q), b = __ldg(J + q);
@@ -92,16 +82,6 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ 
             J2[q] = rb;
             if (MODE == 1) {
                 count(ra.x); count(ra.y); count(ra.z); count(ra.w);
-            } else if (MODE == 2) {
-                atomicAdd(hb + (ra.x & dmask), 1u); atomicAdd(hb + (ra.y & dmask), 1u);
-                atomicAdd(hb + (ra.z & dmask), 1u); atomicAdd(hb + (ra.w & dmask), 1u);
-            }
-        }
-        if (MODE == 2) {
-            __syncthreads();
-            for (int i = threadIdx.x; i <= (int)dmask; i += kRlNT) {
-                H[(uint64_t)i * tiles + t] = hb[i];
-                hb[i] = 0;
             }
         }
     }
@@ -128,20 +108,19 @@ __global__ void k_relabel_scalar(const uint32_t* __restrict__ I, const uint32_t*
 template <int MODE, bool HUBS>
 static void launch_vec(int grid, size_t smem, cudaStream_t s, const uint32_t* I, const uint32_t* J, uint64_t quads,
                        const uint32_t* label, const unsigned long long* hubs, uint32_t n, uint32_t* I2, uint32_t* J2,
-                       uint32_t* counts, uint32_t* H, uint32_t dmask, uint64_t tiles) {
+                       uint32_t* counts) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_relabel<MODE, HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     k_relabel<MODE, HUBS><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs,
-                                                    HubHash::make(n), n, (uint4*)I2, (uint4*)J2, counts, H, dmask,
-                                                    tiles);
+                                                    HubHash::make(n), n, (uint4*)I2, (uint4*)J2, counts);
 }
 
 cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,
                            const unsigned long long* hubs, uint32_t* I2, uint32_t* J2, uint32_t* counts, uint32_t n,
-                           int num_sms, cudaStream_t s, uint32_t* H, int dbits) {
+                           int num_sms, cudaStream_t s) {
     if (counts) {
         cudaError_t err = cudaMemsetAsync(counts, 0, (size_t)n * 4, s);
         if (err != cudaSuccess) return err;
@@ -149,7 +128,6 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
     if (m == 0) return cudaSuccess;
     const bool vec = ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(J) |
                        reinterpret_cast<uintptr_t>(I2) | reinterpret_cast<uintptr_t>(J2)) & 15) == 0;
-    if (H && (!vec || (m & 3) || counts)) return cudaErrorInvalidValue;  // caller falls back to the upsweep
     uint64_t done = 0;
     if (vec && m >= 4) {
         const uint64_t quads = m >> 2;
@@ -161,18 +139,13 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
         // vertices the gathers are DRAM-latency bound and the probe only delays them
         // (c5, n = 2^24: 2.26 ms without, 3.28 ms with).
         if (n > (1u << 23) || getenv("BOBA_NO_HUBS")) hubs = nullptr;
-        const uint32_t dmask = H ? (1u << dbits) - 1u : 0u;
-        const uint64_t tiles = ceil_div(m, 4 * kRlNT);
-        const size_t smem = (hubs ? kHubTableBytes : 0) + 4 * (counts ? kHubHistRows : (H ? 512 : 0));
+        const size_t smem = (hubs ? kHubTableBytes : 0) + 4 * (counts ? kHubHistRows : 0);
         if (counts) {
-            if (hubs) launch_vec<1, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
-            else launch_vec<1, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
-        } else if (H) {
-            if (hubs) launch_vec<2, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
-            else launch_vec<2, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
+            if (hubs) launch_vec<1, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
+            else launch_vec<1, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
         } else {
-            if (hubs) launch_vec<0, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
-            else launch_vec<0, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts, H, dmask, tiles);
+            if (hubs) launch_vec<0, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
+            else launch_vec<0, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
         }
         done = quads * 4;
     }
