@@ -18,6 +18,7 @@ form to build) on the host cores instead.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -562,6 +563,7 @@ def run_sharded(args):
     torch.cuda.synchronize()
     dist.barrier()
     ts = []
+    gc.disable()  # no collector pauses between the host-synchronising collectives of a step
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1)
@@ -573,6 +575,7 @@ def run_sharded(args):
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) / 1e3)
+    gc.enable()
     t = torch.tensor([sum(ts)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_total = float(t.item())
@@ -628,6 +631,7 @@ def run_sharded(args):
                      "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(per_gpu_alg / (ms_step / 1e3) / 1e9 / hbm, 4), "traffic": None,
                      "note": "per-GPU share of SURVEY §8d algorithmic bytes over the whole step incl. collectives"},
+        "step_ms": [round(1e3 * t, 3) for t in ts],
         "cpu_baseline": None,
         "e2e": {"value": round(m / t_e2e / 1e9, 4), "unit": "GEdges/s", "ms_per_step": round(1e3 * t_e2e, 3),
                 "h2d_bytes_per_step": 8 * m, "d2h_bytes_per_step": int(4 * (n + world) + 4 * m),

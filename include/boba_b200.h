@@ -203,6 +203,29 @@ int boba_offset_ids(const uint32_t *in, uint64_t count, uint32_t delta, uint32_t
  * [bounds[p], bounds[p+1]) (bounds: parts+1 ascending device uint32, only
  * bounds[1..parts-1] are read), in input order; counts_out[p] (device) = pairs
  * in part p.  The send side of the multi-GPU all-to-all by row range. */
+/* Compaction of a merged first[] (2 m_global positions) and relabel of a
+ * local edge shard (m edges) with the hub label table the compaction builds
+ * -- phases 2 and 3 of the multi-GPU pipeline (sharded.py), as in the fused
+ * single-GPU call. */
+size_t boba_compact_relabel_workspace_size(uint64_t m_global, uint32_t n);
+int boba_compact_relabel(const uint32_t *first, uint64_t m_global, uint32_t n, const uint32_t *I,
+                         const uint32_t *J, uint64_t m, uint32_t *order, uint32_t *label, uint32_t *I2,
+                         uint32_t *J2, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Row-partitioned CSR across ranks (sharded.py; replaces the reference's
+ * single-process coo_to_csr, graph.py:253-277, for a row range).
+ * boba_adjacent_diff_u32: out[i] = in[i+1] - in[i] for i < count (per-row
+ * counts from CSR offsets).  boba_merge_rows: `recv` holds `parts` senders'
+ * runs back to back in rank order, each run = that sender's entries for rows
+ * [0, rows) in row order with counts[k * rows + r] entries for row r; writes
+ * row r of the output at out_offsets[r] as sender 0's entries, then sender
+ * 1's, ... (global edge order when senders hold contiguous edge shards).
+ * recv_len = the sum of the counts. */
+int boba_adjacent_diff_u32(const uint32_t *in, uint64_t count, uint32_t *out, void *stream);
+size_t boba_merge_rows_workspace_size(int parts, uint32_t rows, uint64_t recv_len);
+int boba_merge_rows(const uint32_t *recv, uint64_t recv_len, int parts, uint32_t rows,
+                    const uint32_t *counts, const uint32_t *out_offsets, uint32_t *out, void *workspace,
+                    size_t workspace_bytes, void *stream);
 size_t boba_range_partition_workspace_size(uint64_t m, int parts);
 int boba_range_partition(const uint32_t *keys, const uint32_t *vals, uint64_t m,
                          const uint32_t *bounds, int parts, uint32_t *keys_out, uint32_t *vals_out,

@@ -59,6 +59,11 @@ SIGNATURES = {
     "boba_ctx_reorder_to_csr_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P], _I),
     "boba_ctx_submit_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_U64)], _I),
     "boba_ctx_wait": ([_P, _U64], _I),
+    "boba_adjacent_diff_u32": ([_P, _U64, _P, _P], _I),
+    "boba_compact_relabel_workspace_size": ([_U64, _U32], _SZ),
+    "boba_compact_relabel": ([_P, _U64, _U32, _P, _P, _U64, _P, _P, _P, _P, _P, _SZ, _P], _I),
+    "boba_merge_rows_workspace_size": ([_I, _U32, _U64], _SZ),
+    "boba_merge_rows": ([_P, _U64, _I, _U32, _P, _P, _P, _P, _SZ, _P], _I),
     "boba_reorder_to_csr_graph_create": ([_P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ,
                                           ctypes.POINTER(_P)], _I),
     "boba_graph_launch": ([_P, _P], _I),

@@ -141,6 +141,28 @@ int boba_order(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, int
     return boba_compact(first, m, n, order, label, nullptr, ws, ws_bytes, stream);
 }
 
+size_t boba_compact_relabel_workspace_size(uint64_t m_global, uint32_t n) {
+    return align256(boba::kHubTableBytes) + boba::compact_workspace_bytes(m_global, n);
+}
+
+int boba_compact_relabel(const uint32_t* first, uint64_t m_global, uint32_t n, const uint32_t* I, const uint32_t* J,
+                         uint64_t m, uint32_t* order, uint32_t* label, uint32_t* I2, uint32_t* J2, void* ws,
+                         size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m_global, n, "boba_compact_relabel")) return rc;
+    if (n == 0) return BOBA_OK;
+    REQUIRE(m <= m_global, "boba_compact_relabel: shard larger than the graph");
+    REQUIRE(first && order && label && ws, "boba_compact_relabel: NULL argument");
+    REQUIRE((I && J && I2 && J2) || m == 0, "boba_compact_relabel: NULL edge arrays");
+    REQUIRE(ws_bytes >= boba_compact_relabel_workspace_size(m_global, n), "boba_compact_relabel: workspace too small");
+    auto* hubs = static_cast<unsigned long long*>(ws);
+    void* rest = static_cast<char*>(ws) + align256(boba::kHubTableBytes);
+    const size_t rest_bytes = ws_bytes - align256(boba::kHubTableBytes);
+    cudaError_t e = boba::launch_compact(first, m_global, n, order, label, nullptr, hubs, rest, rest_bytes, num_sms(),
+                                         S(stream));
+    if (e == cudaSuccess) e = boba::launch_relabel(I, J, m, label, hubs, I2, J2, nullptr, n, num_sms(), S(stream));
+    return cuda_status(e, "boba_compact_relabel");
+}
+
 int boba_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, const uint32_t* label, uint32_t* I2,
                  uint32_t* J2, uint32_t* row_counts, void* stream) {
     if (int rc = check_sizes(m, n, "boba_relabel")) return rc;
@@ -467,6 +489,27 @@ int boba_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m,
     return cuda_status(boba::launch_range_partition(keys, vals, m, bounds, parts, keys_out, vals_out, counts_out, ws,
                                                     ws_bytes, num_sms(), S(stream)),
                        "boba_range_partition");
+}
+
+int boba_adjacent_diff_u32(const uint32_t* in, uint64_t count, uint32_t* out, void* stream) {
+    REQUIRE((in && out) || count == 0, "boba_adjacent_diff_u32: NULL argument");
+    return cuda_status(boba::launch_adjacent_diff(in, count, out, num_sms(), S(stream)), "boba_adjacent_diff_u32");
+}
+
+size_t boba_merge_rows_workspace_size(int parts, uint32_t rows, uint64_t recv_len) {
+    return boba::merge_rows_workspace_bytes(parts, rows, recv_len);
+}
+
+int boba_merge_rows(const uint32_t* recv, uint64_t recv_len, int parts, uint32_t rows, const uint32_t* counts,
+                    const uint32_t* out_offsets, uint32_t* out, void* ws, size_t ws_bytes, void* stream) {
+    REQUIRE(parts >= 1, "boba_merge_rows: parts must be positive");
+    REQUIRE((uint64_t)parts * rows < 0xFFFFFFFFull && recv_len < 0xFFFFFFFFull, "boba_merge_rows: too large");
+    REQUIRE(ws && (rows == 0 || (counts && out_offsets)), "boba_merge_rows: NULL argument");
+    REQUIRE((recv && out) || recv_len == 0, "boba_merge_rows: NULL entries");
+    REQUIRE(ws_bytes >= boba::merge_rows_workspace_bytes(parts, rows, recv_len), "boba_merge_rows: workspace too small");
+    return cuda_status(boba::launch_merge_rows(recv, recv_len, parts, rows, counts, out_offsets, out, ws, ws_bytes,
+                                               num_sms(), S(stream)),
+                       "boba_merge_rows");
 }
 
 int boba_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, void* stream) {

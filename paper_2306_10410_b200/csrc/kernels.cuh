@@ -78,4 +78,12 @@ cudaError_t launch_pagerank(const uint32_t* offsets, const uint32_t* indices, co
 cudaError_t launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, int num_sms,
                               cudaStream_t s);
 
+// multi-GPU row-partitioned CSR (shard.cu)
+cudaError_t launch_adjacent_diff(const uint32_t* in, uint64_t count, uint32_t* out, int num_sms, cudaStream_t s);
+size_t merge_rows_workspace_bytes(int parts, uint32_t rows, uint64_t recv_len);
+// recv_len must equal the sum of counts
+cudaError_t launch_merge_rows(const uint32_t* recv, uint64_t recv_len, int parts, uint32_t rows,
+                              const uint32_t* counts, const uint32_t* out_off, uint32_t* out, void* ws,
+                              size_t ws_bytes, int num_sms, cudaStream_t s);
+
 }  // namespace boba

@@ -12,12 +12,15 @@ holds edges [e0_k, e0_k + m_k) of the global edge list, in order:
   P2  rank compaction, replicated on every rank (O(n + m/32) work, no
       communication): order and label are identical everywhere.
   P3  relabel of the local shard against the replicated label.
-  P4  global row histogram (allreduce-SUM) -> global CSR offsets; rows are cut
-      into P ranges of ~m/P edges; each rank stably partitions its shard by
-      destination range (boba_range_partition) and an all-to-all delivers
-      every edge to the owner of its row.  Receivers get sender chunks in rank
-      order and each chunk in shard order, i.e. global edge order, so the
-      local stable COO->CSR reproduces the reference's within-row order.
+  P4  each rank builds the stable CSR of its shard over all n rows (the
+      one-GPU COO->CSR); the sum of the local offsets arrays (allreduce-SUM)
+      is the global offsets array.  Rows are cut into P ranges of ~m/P edges.
+      The edges rank j owes the owner of rows [b_k, b_k+1) are one contiguous
+      run of its local indices, so one all-to-all of column ids (4 bytes per
+      edge) and one of per-row counts deliver them; the owner interleaves the
+      runs row by row in rank order (boba_merge_rows).  Shards are contiguous
+      in edge order, so that is global edge order: the reference's
+      within-row order, bit-exact.
   P5  row-partitioned SpMV; x replicated (allgather of y slices to iterate).
 
 The algorithm is written against a small ``ops`` object (DeviceOps below:
@@ -60,6 +63,17 @@ class DeviceOps:
     def relabel(self, I, J, label, n: int):
         return D.relabel(I, J, label, n)
 
+    def compact_relabel(self, first, I, J, m_global: int, n: int):
+        """P2 + P3 with the hub label table, as in the fused one-GPU call."""
+        dev = I.device
+        m = I.numel()
+        e = lambda k: torch.empty(max(k, 1), dtype=D.ID, device=dev)[:k]  # noqa: E731
+        order, label, I2, J2 = e(n), e(n), e(m), e(m)
+        ws = D._ws(N.lib.boba_compact_relabel_workspace_size(m_global, n), dev)
+        N.check(N.lib.boba_compact_relabel(D._p(first), m_global, n, D._p(I), D._p(J), m, D._p(order), D._p(label),
+                                           D._p(I2), D._p(J2), D._p(ws), ws.numel(), D._s()))
+        return order, label, I2, J2
+
     def degrees(self, I2, n: int):
         return D.degrees(I2, n)
 
@@ -87,6 +101,19 @@ class DeviceOps:
     def coo_to_csr(self, rows, cols, n_rows: int):
         offsets, indices, _ = D.coo_to_csr(rows, cols, n_rows)
         return offsets, indices
+
+    def adjacent_diff(self, t):
+        out = torch.empty(max(t.numel() - 1, 1), dtype=D.ID, device=t.device)[: t.numel() - 1]
+        N.check(N.lib.boba_adjacent_diff_u32(D._p(t), t.numel() - 1, D._p(out), D._s()))
+        return out
+
+    def merge_rows(self, recv, counts, parts: int, rows: int, out_offsets):
+        total = recv.numel()
+        out = torch.empty(max(total, 1), dtype=D.ID, device=recv.device)[:total]
+        ws = D._ws(N.lib.boba_merge_rows_workspace_size(parts, rows, total), recv.device)
+        N.check(N.lib.boba_merge_rows(D._p(recv), total, parts, rows, D._p(counts), D._p(out_offsets), D._p(out),
+                                      D._p(ws), ws.numel(), D._s()))
+        return out
 
 
 @dataclass
@@ -136,26 +163,31 @@ def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: i
     key = ops.bias(first)
     dist.all_reduce(key, op=_MIN, group=group)
     first = ops.bias(key)
-    # P2: replicated compaction
-    order, label = ops.compact(first, m_global, n)
-    # P3: local relabel
-    I2, J2 = ops.relabel(I, J, label, n)
-    # P4: global row histogram -> offsets -> edge-balanced row ranges
-    counts = ops.degrees(I2, n)
-    dist.all_reduce(counts, op=_SUM, group=group)
-    offsets_g = ops.exclusive_scan(counts)
+    # P2: replicated compaction; P3: local relabel
+    order, label, I2, J2 = ops.compact_relabel(first, I, J, m_global, n)
+    # P4: local CSR of the shard over all n rows; global offsets = sum of the local ones
+    loc_off, loc_idx = ops.coo_to_csr(I2, J2, n)
+    offsets_g = loc_off.clone()
+    dist.all_reduce(offsets_g, op=_SUM, group=group)
     bounds64 = row_bounds(offsets_g, m_global, P)
-    bounds = bounds64.to(torch.int32)
-    keys, vals, part_counts = ops.range_partition(I2, J2, bounds, P)
-    recv_counts_t = torch.empty_like(part_counts)
-    dist.all_to_all_single(recv_counts_t, part_counts, group=group)
-    send_counts = [int(c) for c in part_counts.cpu().tolist()]
-    recv_counts = [int(c) for c in recv_counts_t.cpu().tolist()]
-    rkeys = _alltoallv(keys, send_counts, recv_counts, group)
-    rvals = _alltoallv(vals, send_counts, recv_counts, group)
-    lo, hi = int(bounds64[r]), int(bounds64[r + 1])
-    rows = ops.offset_ids(rkeys, -lo)
-    offsets, indices = ops.coo_to_csr(rows, rvals, hi - lo)
+    b = [int(x) for x in bounds64.cpu().tolist()]
+    cut = (loc_off.to(torch.int64) & 0xFFFFFFFF)[bounds64].cpu().tolist()     # local run ends per owner
+    send_counts = [int(cut[k + 1] - cut[k]) for k in range(P)]
+    send_t = torch.tensor(send_counts, dtype=torch.int64, device=I.device)
+    recv_t = torch.empty_like(send_t)
+    dist.all_to_all_single(recv_t, send_t, group=group)
+    recv_counts = [int(c) for c in recv_t.cpu().tolist()]
+    lo, hi = b[r], b[r + 1]
+    rows_of = [b[k + 1] - b[k] for k in range(P)]
+    # per-row counts: owners' row ranges tile [0, n) in rank order, so the send
+    # buffer is simply the whole local count array
+    row_counts = ops.adjacent_diff(loc_off)
+    recv_rc = _alltoallv(row_counts, rows_of, [hi - lo] * P, group)
+    recv_idx = _alltoallv(loc_idx, send_counts, recv_counts, group)
+    g_lo = int((offsets_g[lo:lo + 1].to(torch.int64) & 0xFFFFFFFF).item())
+    offsets = ops.offset_ids(offsets_g[lo:hi + 1].contiguous(), -g_lo)
+    # one rank: its run is already the whole CSR
+    indices = recv_idx if P == 1 else ops.merge_rows(recv_idx, recv_rc, P, hi - lo, offsets)
     return ShardResult(first, order, label, I2, J2, lo, hi, offsets, indices, offsets_g)
 
 

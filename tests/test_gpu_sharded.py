@@ -71,6 +71,35 @@ def test_range_partition_and_helpers(ops):
     assert np.array_equal(host(ops.exclusive_scan(cu(counts))), u32(npo.exclusive_scan(t32(counts))))
 
 
+@pytest.mark.parametrize("P", [1, 3, 8])
+def test_merge_rows_matches_twin(ops, P):
+    """Receiver side of the row-range all-to-all: P senders' local CSRs of
+    contiguous edge shards, restricted to one owner's row range, interleaved
+    row by row in rank order == the single-process CSR of those rows."""
+    from paper_2306_10410_b200.sharded import shard_range
+
+    I, J = oracle.rmat_edges(13, 8, seed=11)
+    n, m = 1 << 13, I.size
+    _, _, _, _, off, idx, _ = oracle.pipeline(I, J, n)
+    off_g, idx_g = oracle.coo_to_csr(I, J, n)[:2]
+    lo, hi = 1000, 5000                                   # this owner's rows
+    npo = NumpyOps()
+    runs, rcs = [], []
+    for k in range(P):
+        e0, e1 = shard_range(m, k, P)
+        lo_off, lo_idx = ops.coo_to_csr(cu(I[e0:e1]), cu(J[e0:e1]), n)
+        rc = ops.adjacent_diff(lo_off)
+        assert np.array_equal(host(rc), u32(npo.adjacent_diff(t32(host(lo_off)))))
+        o = host(lo_off).astype(np.int64)
+        runs.append(host(lo_idx)[o[lo]:o[hi]])
+        rcs.append(host(rc)[lo:hi])
+    recv, counts = np.concatenate(runs), np.concatenate(rcs)
+    out_off = (off_g[lo:hi + 1] - off_g[lo]).astype(np.uint32)
+    got = host(ops.merge_rows(cu(recv), cu(counts), P, hi - lo, cu(out_off)))
+    assert np.array_equal(got, u32(npo.merge_rows(t32(recv), t32(counts), P, hi - lo, t32(out_off))))
+    assert np.array_equal(got, idx_g[off_g[lo]:off_g[hi]].astype(np.uint32))
+
+
 def test_sharded_pipeline_one_rank_nccl(ops):
     import torch
     import torch.distributed as dist

@@ -51,6 +51,10 @@ class NumpyOps:
         lab = u32(label)
         return t32(lab[u32(I)]), t32(lab[u32(J)])
 
+    def compact_relabel(self, first, I, J, m_global, n):
+        order, label = self.compact(first, m_global, n)
+        return (order, label) + self.relabel(I, J, label, n)
+
     def degrees(self, I2, n):
         return t32(np.bincount(u32(I2), minlength=n))
 
@@ -73,6 +77,22 @@ class NumpyOps:
         o = np.argsort(r, kind="stable")
         off = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=n_rows))])
         return t32(off), t32(c[o])
+
+    def adjacent_diff(self, t):
+        a = u32(t).astype(np.int64)
+        return t32((a[1:] - a[:-1]) & 0xFFFFFFFF)
+
+    def merge_rows(self, recv, counts, parts, rows, out_offsets):
+        rv, cnt = u32(recv), u32(counts).astype(np.int64).reshape(parts, rows)
+        off = u32(out_offsets).astype(np.int64)
+        src = np.concatenate([[0], np.cumsum(cnt.ravel())])[:-1].reshape(parts, rows)
+        out = np.empty(rv.size, dtype=U32)
+        for r in range(rows):
+            d = off[r]
+            for k in range(parts):
+                out[d:d + cnt[k, r]] = rv[src[k, r]:src[k, r] + cnt[k, r]]
+                d += cnt[k, r]
+        return t32(out)
 
 
 def _worker(rank, world, port, cases, outdir):
