@@ -244,7 +244,9 @@ int boba_reorder_to_csr_timed(const uint32_t* I, const uint32_t* J, const double
     const int sms = num_sms();
     mark(0);
     // the hub table area doubles as phase 1's SeenSet (dead before phase 2 refills it)
-    cudaError_t e = boba::launch_first_hit_shard(I, J, m, m, 0, n, first, false, hubs, sms, s);
+    // the compaction workspace (`rest`, >= 2m bits) is idle during phase 1: it holds the wave bitmaps
+    void* bits_ws = rest_bytes >= boba::first_hit_bits_workspace_bytes(n) ? rest : nullptr;
+    cudaError_t e = boba::launch_first_hit_shard(I, J, m, m, 0, n, first, false, hubs, sms, s, bits_ws);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: first occurrence");
     mark(1);
     e = boba::launch_compact(first, m, n, order, label, nullptr, hubs, rest, rest_bytes, sms, s);

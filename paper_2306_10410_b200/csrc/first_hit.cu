@@ -130,15 +130,28 @@ __device__ __forceinline__ uint32_t ld_cg_pred(const uint32_t* p, bool pred) {
                  : "l"(p), "r"((uint32_t)pred));
     return r;
 }
+__device__ __forceinline__ void red_or_pred(uint32_t* p, uint32_t v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.relaxed.gpu.global.or.b32 [%0], %1;\n\t}" ::"l"(p),
+                 "r"(v), "r"((uint32_t)pred)
+                 : "memory");
+}
 __device__ __forceinline__ void red_min_pred(uint32_t* p, uint32_t v, bool pred) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.relaxed.gpu.global.min.u32 [%0], %1;\n\t}" ::"l"(p),
                  "r"(v), "r"((uint32_t)pred)
                  : "memory");
 }
 
-template <int TW>
+// BITS (first[] beyond L2, n > 2^23): the guard is not a load of first[v]
+// (a DRAM line per access) but a bit of `seenb` (n bits, L2-resident): the
+// vertices whose first occurrence lies in an earlier WAVE of positions.  A
+// position passes to the red.min only for vertices not seen before its wave,
+// and marks them in `newb`, which joins `seenb` after the wave (a bit set
+// inside the wave would let a later position hide an earlier one still in
+// flight).
+template <int TW, bool BITS>
 __device__ __forceinline__ void sweep_static(const uint4* __restrict__ src, uint64_t nq, uint32_t base,
-                                             uint32_t* first, const unsigned long long* set, const HubHash& hh) {
+                                             uint32_t* first, const unsigned long long* set, const HubHash& hh,
+                                             const uint32_t* __restrict__ seenb, uint32_t* newb) {
     constexpr uint64_t kIter = (uint64_t)kFhNT * kFhQuads;
     const uint64_t iters = ceil_div(nq, kIter);
     for (uint64_t it = blockIdx.x; it < iters; it += gridDim.x) {
@@ -163,39 +176,60 @@ __device__ __forceinline__ void sweep_static(const uint4* __restrict__ src, uint
         for (int k = 0; k < kFhQuads; k++) {
             const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
 #pragma unroll
-            for (int j = 0; j < 4; j++) cur[k][j] = ld_cg_pred(first + vs[j], need[k][j]);
+            for (int j = 0; j < 4; j++)
+                cur[k][j] = BITS ? ld_cg_pred(seenb + (vs[j] >> 5), need[k][j]) : ld_cg_pred(first + vs[j], need[k][j]);
         }
 #pragma unroll
         for (int k = 0; k < kFhQuads; k++) {
             const uint32_t vs[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
             const uint32_t p0 = base + 4u * (uint32_t)(q0 + (uint64_t)k * kFhNT);
 #pragma unroll
-            for (int j = 0; j < 4; j++) red_min_pred(first + vs[j], p0 + j, need[k][j] && p0 + j < cur[k][j]);
+            for (int j = 0; j < 4; j++) {
+                if (BITS) {
+                    const bool go = need[k][j] && !((cur[k][j] >> (vs[j] & 31)) & 1u);
+                    red_min_pred(first + vs[j], p0 + j, go);
+                    red_or_pred(newb + (vs[j] >> 5), 1u << (vs[j] & 31), go);
+                } else {
+                    red_min_pred(first + vs[j], p0 + j, need[k][j] && p0 + j < cur[k][j]);
+                }
+            }
         }
     }
 }
 
-template <int TW>
+template <int TW, bool BITS>
 __global__ void __launch_bounds__(kFhNT, 1) k_first_hit_static(Ranges r, uint32_t* first,
                                                                const unsigned long long* __restrict__ seen_g,
-                                                               HubHash hh) {
+                                                               HubHash hh, const uint32_t* seenb, uint32_t* newb) {
     extern __shared__ unsigned long long smem_u64[];
     for (int i = threadIdx.x; i < kHubBuckets; i += kFhNT) smem_u64[i] = __ldg(seen_g + i);
     __syncthreads();
-    sweep_static<TW>(reinterpret_cast<const uint4*>(r.a), r.qa, r.base_a, first, smem_u64, hh);
-    sweep_static<TW>(reinterpret_cast<const uint4*>(r.b), r.qb, r.base_b, first, smem_u64, hh);
+    sweep_static<TW, BITS>(reinterpret_cast<const uint4*>(r.a), r.qa, r.base_a, first, smem_u64, hh, seenb, newb);
+    sweep_static<TW, BITS>(reinterpret_cast<const uint4*>(r.b), r.qb, r.base_b, first, smem_u64, hh, seenb, newb);
 }
 
-template <int TW>
+template <int TW, bool BITS = false>
 static void launch_static(const Ranges& r, uint32_t* first, const unsigned long long* seen_g, const HubHash& hh,
-                          int num_sms, cudaStream_t s) {
+                          int num_sms, cudaStream_t s, const uint32_t* seenb = nullptr, uint32_t* newb = nullptr) {
     const size_t smem = sizeof(unsigned long long) * kHubBuckets;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_first_hit_static<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_first_hit_static<TW, BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_first_hit_static<TW><<<num_sms, kFhNT, smem, s>>>(r, first, seen_g, hh);
+    k_first_hit_static<TW, BITS><<<num_sms, kFhNT, smem, s>>>(r, first, seen_g, hh, seenb, newb);
+}
+
+// seenb |= newb; newb = 0 (between waves)
+__global__ void k_merge_bits(uint32_t* seenb, uint32_t* newb, uint64_t words) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) {
+        const uint32_t b = newb[i];
+        if (b) {
+            seenb[i] |= b;
+            newb[i] = 0;
+        }
+    }
 }
 
 // SeenSet from the prefix: every vertex whose first occurrence is one of the
@@ -267,9 +301,42 @@ size_t first_hit_workspace_bytes() { return kHubTableBytes; }
 // A contiguous shard [e0, e0 + m) of a global edge list with m_global edges:
 // local I[i] sits at global position e0 + i, local J[i] at m_global + e0 + i.
 // `seen_ws` (kHubTableBytes, may be NULL) enables the two-stage sweep.
+size_t first_hit_bits_workspace_bytes(uint32_t n) { return 2 * (((uint64_t)n + 31) / 32 * 4 + 256); }
+
+// Static sweep of r in waves of kFhWave positions (BITS mode, see sweep_static).
+constexpr uint64_t kFhWaveQuads = (1ull << 26) / 4;
+
+template <int TW>
+static cudaError_t launch_static_waves(const Ranges& r, uint32_t* first, const unsigned long long* set,
+                                       const HubHash& hh, uint32_t n, void* bits_ws, int num_sms, cudaStream_t s) {
+    const uint64_t words = ((uint64_t)n + 31) / 32;
+    uint32_t* seenb = static_cast<uint32_t*>(bits_ws);
+    uint32_t* newb = reinterpret_cast<uint32_t*>(static_cast<char*>(bits_ws) + (words * 4 + 256) / 256 * 256);
+    cudaError_t e = cudaMemsetAsync(seenb, 0, words * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(newb, 0, words * 4, s);
+    if (e != cudaSuccess) return e;
+    const uint64_t total = r.qa + r.qb;
+    const uint64_t mb = ceil_div(words, 256), cap = (uint64_t)num_sms * 8;
+    for (uint64_t w0 = 0; w0 < total; w0 += kFhWaveQuads) {
+        const uint64_t w1 = w0 + kFhWaveQuads < total ? w0 + kFhWaveQuads : total;
+        Ranges rw{};
+        const uint64_t a0 = w0 < r.qa ? w0 : r.qa, a1 = w1 < r.qa ? w1 : r.qa;  // part in A
+        rw.a = r.a + 4 * a0;
+        rw.qa = a1 - a0;
+        rw.base_a = r.base_a + (uint32_t)(4 * a0);
+        const uint64_t b0 = w0 > r.qa ? w0 - r.qa : 0, b1 = w1 > r.qa ? w1 - r.qa : 0;  // part in B
+        rw.b = r.b + 4 * b0;
+        rw.qb = b1 - b0;
+        rw.base_b = r.base_b + (uint32_t)(4 * b0);
+        launch_static<TW, true>(rw, first, set, hh, num_sms, s, seenb, newb);
+        if (w1 < total) k_merge_bits<<<(unsigned)(mb < cap ? mb : cap), 256, 0, s>>>(seenb, newb, words);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_t m, uint64_t m_global, uint64_t e0,
                                    uint32_t n, uint32_t* first, bool relaxed, void* seen_ws, int num_sms,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, void* bits_ws) {
     const uint32_t base_i = (uint32_t)e0, base_j = (uint32_t)(m_global + e0);
     cudaError_t err = cudaMemsetAsync(first, 0xFF, (size_t)n * sizeof(uint32_t), s);
     if (err != cudaSuccess || m == 0) return err;
@@ -288,13 +355,19 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
             err = cudaMemsetAsync(set, 0xFF, kHubTableBytes, s);
             if (err != cudaSuccess) return err;
             Ranges r2{I + prefix, quads - qp, base_i + prefix, J, quads, base_j};
+            // first[] beyond L2 (n > 2^24, > 64 MB): guard on a seen-bitmap in waves instead of
+            // first[] itself (measured: s26 18.0 -> 9.3 ms; s24, table still partly in L2: 1.90 vs 2.35)
+            const bool waves = bits_ws && n > (1u << 24);
             if (hh.tag_bits <= 8) {
                 k_seen_build<8><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
-                launch_static<8>(r2, first, set, hh, num_sms, s);
+                if (waves) err = launch_static_waves<8>(r2, first, set, hh, n, bits_ws, num_sms, s);
+                else launch_static<8>(r2, first, set, hh, num_sms, s);
             } else {
                 k_seen_build<16><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
-                launch_static<16>(r2, first, set, hh, num_sms, s);
+                if (waves) err = launch_static_waves<16>(r2, first, set, hh, n, bits_ws, num_sms, s);
+                else launch_static<16>(r2, first, set, hh, num_sms, s);
             }
+            if (err != cudaSuccess) return err;
         } else {
             Ranges r{I, quads, base_i, J, quads, base_j};
             if (relaxed)

@@ -12,9 +12,12 @@ cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, u
 
 // seen_ws (first_hit_workspace_bytes(), may be NULL) enables the two-stage sweep
 size_t first_hit_workspace_bytes();
+// bits_ws (first_hit_bits_workspace_bytes(n), may be NULL): for n > 2^24 the
+// two-stage sweep then guards on an L2-resident seen-bitmap in waves
+size_t first_hit_bits_workspace_bytes(uint32_t n);
 cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_t m, uint64_t m_global, uint64_t e0,
                                    uint32_t n, uint32_t* first, bool relaxed, void* seen_ws, int num_sms,
-                                   cudaStream_t s);
+                                   cudaStream_t s, void* bits_ws = nullptr);
 
 size_t compact_workspace_bytes(uint64_t m, uint32_t n);
 // hubs (may be NULL): kHubTableBytes table filled for phase 3 (hubs.cuh)
