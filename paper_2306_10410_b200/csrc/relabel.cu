@@ -30,7 +30,17 @@ constexpr int kHubHistRows = 8192;
 // np.bincount of graph.py:270).  (Also writing the first radix pass's tile
 // histogram here was measured: the per-tile barrier it needs costs more in
 // this latency-bound loop than the upsweep it saves.)
-template <int MODE, bool HUBS>
+// STREAM (label[] beyond L2): the edge streams are loaded and stored
+// evict-first and the label gathers marked evict-last, so the 17 GB of
+// streaming traffic at s26 does not push the table's lines out of L2.
+__device__ __forceinline__ uint32_t ld_label(const uint32_t* p, bool stream, unsigned long long pol) {
+    if (!stream) return __ldcg(p);
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+template <int MODE, bool HUBS, bool STREAM = false>
 __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ I, const uint4* __restrict__ J,
                                                       uint64_t quads, const uint32_t* __restrict__ label,
                                                       const unsigned long long* __restrict__ hubs, HubHash hh,
@@ -61,9 +71,11 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ 
         }
         return 0xFFFFFFFFu;
     };
+    unsigned long long pol = 0;
+    if (STREAM) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     auto lookup = [&](uint32_t v) -> uint32_t {
         const uint32_t h = probe(v);
-        return h != 0xFFFFFFFFu ? h : __ldcg(label + v);
+        return h != 0xFFFFFFFFu ? h : ld_label(label + v, STREAM, pol);
     };
     auto count = [&](uint32_t r) {
         if (r < (uint32_t)kHubHistRows)
@@ -74,12 +86,17 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ 
     for (uint64_t t = blockIdx.x; t * kRlNT < quads; t += gridDim.x) {
         const uint64_t q = t * kRlNT + threadIdx.x;
         if (q < quads) {
-            const uint4 a = __ldg(I + q), b = __ldg(J + q);
+            const uint4 a = STREAM ? __ldcs(I + q) : __ldg(I + q), b = STREAM ? __ldcs(J + q) : __ldg(J + q);
             uint4 ra, rb;
             ra.x = lookup(a.x); ra.y = lookup(a.y); ra.z = lookup(a.z); ra.w = lookup(a.w);
             rb.x = lookup(b.x); rb.y = lookup(b.y); rb.z = lookup(b.z); rb.w = lookup(b.w);
-            I2[q] = ra;
-            J2[q] = rb;
+            if (STREAM) {
+                __stcs(I2 + q, ra);
+                __stcs(J2 + q, rb);
+            } else {
+                I2[q] = ra;
+                J2[q] = rb;
+            }
             if (MODE == 1) {
                 count(ra.x); count(ra.y); count(ra.z); count(ra.w);
             }
@@ -105,16 +122,16 @@ __global__ void k_relabel_scalar(const uint32_t* __restrict__ I, const uint32_t*
     }
 }
 
-template <int MODE, bool HUBS>
+template <int MODE, bool HUBS, bool STREAM = false>
 static void launch_vec(int grid, size_t smem, cudaStream_t s, const uint32_t* I, const uint32_t* J, uint64_t quads,
                        const uint32_t* label, const unsigned long long* hubs, uint32_t n, uint32_t* I2, uint32_t* J2,
                        uint32_t* counts) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_relabel<MODE, HUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_relabel<MODE, HUBS, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_relabel<MODE, HUBS><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs,
+    k_relabel<MODE, HUBS, STREAM><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs,
                                                     HubHash::make(n), n, (uint4*)I2, (uint4*)J2, counts);
 }
 
@@ -143,6 +160,10 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
         if (counts) {
             if (hubs) launch_vec<1, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
             else launch_vec<1, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
+        } else if (n > (1u << 24)) {
+            // measured at s26: 22.6 -> 21.8 ms (with the hub table in shared memory instead: 25.1 ms --
+            // it leaves the L1, which holds the hot labels here, only ~36 KB)
+            launch_vec<0, false, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
         } else {
             if (hubs) launch_vec<0, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
             else launch_vec<0, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
