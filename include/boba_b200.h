@@ -181,6 +181,14 @@ int boba_ctx_submit_host(boba_ctx *ctx, const uint32_t *I_host, const uint32_t *
                          uint64_t *ticket);
 int boba_ctx_wait(boba_ctx *ctx, uint64_t ticket);
 
+/* --- Locality metric (reference metrics.py:90-115 nbr) -------------------
+ * Mean over rows with neighbours of (distinct index / line_size lines) /
+ * (row degree); *out is a device double.  m and n must be positive
+ * (the reference raises UndefinedMetricError without edges). */
+size_t boba_nbr_workspace_size(uint64_t m, uint32_t n);
+int boba_nbr(const uint32_t *offsets, const uint32_t *indices, uint32_t n, uint64_t m, uint32_t line_size,
+             double *out, void *workspace, size_t workspace_bytes, void *stream);
+
 /* --- Plumbing and input generators --------------------------------------- */
 /* int64 -> uint32 with the reference's range check (graph.py:99-106):
  * returns BOBA_ERANGE and *bad_index (host, may be NULL) = first offending

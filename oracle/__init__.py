@@ -256,3 +256,23 @@ def pipeline(I, J, n, threads=0, weights=None):
     I2, J2 = apply_permutation(I, J, label)
     offsets, indices, w2 = coo_to_csr(I2, J2, n, weights)
     return order, label, I2, J2, offsets, indices, w2
+
+
+def nbr(offsets, indices, line_size=32):
+    """reference metrics.py:90-115 (neighbourhood line ratio), restated in
+    numpy: per row with neighbours, distinct index // line_size values over
+    the degree; the mean of those ratios."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    indices = np.asarray(indices, dtype=np.int64)
+    n = offsets.size - 1
+    deg = np.diff(offsets)
+    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
+    lines = indices // line_size
+    k = np.lexsort((lines, rows))
+    rs, ls = rows[k], lines[k]
+    boundary = np.empty(rs.size, dtype=bool)
+    boundary[0] = True
+    boundary[1:] = (rs[1:] != rs[:-1]) | (ls[1:] != ls[:-1])
+    counts = np.bincount(rs[boundary], minlength=n)
+    mask = deg > 0
+    return float(np.mean(counts[mask] / deg[mask]))

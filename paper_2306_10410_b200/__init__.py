@@ -13,6 +13,7 @@ from .errors import BobaError, MalformedGraphError, ParseError, UndefinedMetricE
 from .graph import (CooGraph, CsrGraph, Permutation, apply_permutation, coo_to_csr, degrees, sort_coo_by_destination,
                     total_degrees)
 from .kernels import pagerank, spmv_pull
+from .metrics import nbr
 from .ordering import (
     ORDERING_CHOICES,
     RANK_UNSET,
@@ -36,7 +37,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BobaError", "MalformedGraphError", "ParseError", "UndefinedMetricError",
     "CooGraph", "CsrGraph", "Permutation", "apply_permutation", "coo_to_csr", "degrees",
-    "total_degrees", "sort_coo_by_destination", "spmv_pull", "pagerank", "RANK_UNSET", "ORDERING_CHOICES", "boba_parallel", "boba_sequential",
+    "total_degrees", "sort_coo_by_destination", "spmv_pull", "pagerank", "nbr", "RANK_UNSET", "ORDERING_CHOICES", "boba_parallel", "boba_sequential",
     "compute_ordering", "random_order", "identity_order", "degree_order", "hub_order", "BobaOrder", "RandomOrder",
     "IdentityOrder", "DegreeOrder", "HubOrder",
     "__version__",

@@ -142,3 +142,11 @@ def pagerank(offsets, indices, n: int, weights, damping: float, tol: float, max_
     dw = None if weights is None else torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
     x, it = D.pagerank(do, di, dw, damping, tol, max_iters)
     return x.cpu().numpy(), int(it.cpu()[0])
+
+
+def nbr(offsets, indices, line_size: int) -> float:
+    n = int(np.asarray(offsets).size) - 1
+    m = int(np.asarray(indices).size)
+    do = to_device_ids(offsets, m + 1, "offsets")
+    di = to_device_ids(indices, max(n, 1), "indices")
+    return D.nbr(do, di, line_size)

@@ -60,6 +60,8 @@ SIGNATURES = {
     "boba_ctx_submit_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_U64)], _I),
     "boba_ctx_wait": ([_P, _U64], _I),
     "boba_adjacent_diff_u32": ([_P, _U64, _P, _P], _I),
+    "boba_nbr_workspace_size": ([_U64, _U32], _SZ),
+    "boba_nbr": ([_P, _P, _U32, _U64, _U32, _P, _P, _SZ, _P], _I),
     "boba_compact_relabel_workspace_size": ([_U64, _U32], _SZ),
     "boba_compact_relabel": ([_P, _U64, _U32, _P, _P, _U64, _P, _P, _P, _P, _P, _SZ, _P], _I),
     "boba_merge_rows_workspace_size": ([_I, _U32, _U64], _SZ),

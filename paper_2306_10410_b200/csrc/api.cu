@@ -585,6 +585,19 @@ int boba_pagerank(const uint32_t* offsets, const uint32_t* indices, const double
                        "boba_pagerank");
 }
 
+size_t boba_nbr_workspace_size(uint64_t m, uint32_t n) { return boba::nbr_workspace_bytes(m, n); }
+
+int boba_nbr(const uint32_t* offsets, const uint32_t* indices, uint32_t n, uint64_t m, uint32_t line_size,
+             double* out, void* ws, size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_nbr")) return rc;
+    REQUIRE(line_size >= 1, "line size must be at least 1, got %u", line_size);
+    REQUIRE(m > 0 && n > 0, "boba_nbr: the neighbourhood line ratio is undefined without edges");
+    REQUIRE(offsets && indices && out && ws, "boba_nbr: NULL argument");
+    REQUIRE(ws_bytes >= boba::nbr_workspace_bytes(m, n), "boba_nbr: workspace too small");
+    return cuda_status(boba::launch_nbr(offsets, indices, n, m, line_size, out, ws, ws_bytes, num_sms(), S(stream)),
+                       "boba_nbr");
+}
+
 int boba_generate_rmat(int scale, uint64_t m, uint64_t seed, uint32_t* I, uint32_t* J, void* stream) {
     REQUIRE(scale >= 0 && scale <= 32, "boba_generate_rmat: scale out of range");
     REQUIRE((I && J) || m == 0, "boba_generate_rmat: NULL argument");

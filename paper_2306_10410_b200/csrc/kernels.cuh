@@ -81,6 +81,11 @@ cudaError_t launch_pagerank(const uint32_t* offsets, const uint32_t* indices, co
 cudaError_t launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, int num_sms,
                               cudaStream_t s);
 
+// neighbourhood line ratio (metrics.cu); out: device double
+size_t nbr_workspace_bytes(uint64_t m, uint32_t n);
+cudaError_t launch_nbr(const uint32_t* offsets, const uint32_t* indices, uint32_t n, uint64_t m, uint32_t line_size,
+                       double* out, void* ws, size_t ws_bytes, int num_sms, cudaStream_t s);
+
 // multi-GPU row-partitioned CSR (shard.cu)
 cudaError_t launch_adjacent_diff(const uint32_t* in, uint64_t count, uint32_t* out, int num_sms, cudaStream_t s);
 size_t merge_rows_workspace_bytes(int parts, uint32_t rows, uint64_t recv_len);

@@ -187,6 +187,16 @@ def pagerank(offsets: torch.Tensor, indices: torch.Tensor, weights: torch.Tensor
     return x, iters
 
 
+def nbr(offsets: torch.Tensor, indices: torch.Tensor, line_size: int = 32) -> float:
+    """Neighbourhood line ratio (reference metrics.py:90-115) on device CSR."""
+    n = offsets.numel() - 1
+    m = indices.numel()
+    out = torch.empty(1, dtype=torch.float64, device=offsets.device)
+    ws = _ws(N.lib.boba_nbr_workspace_size(m, n), offsets.device)
+    N.check(N.lib.boba_nbr(_p(offsets), _p(indices), n, m, line_size, _p(out), _p(ws), ws.numel(), _s()))
+    return float(out.item())
+
+
 def spmv_workspace(n: int, m: int, device) -> torch.Tensor:
     return _ws(N.lib.boba_spmv_workspace_size(n, m), device)
 

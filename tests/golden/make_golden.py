@@ -20,6 +20,8 @@ fuzz.npz     random_coo multigraphs from the reference's own fuzz seeds
 medium.npz   R-MAT s12 ef8 (repo generator), grid 64x64 and LCD(5000,4)
              (reference generator), each randomly relabelled with the
              reference's randomize_labels; outputs stored whole
+Every case also stores the reference's neighbourhood line ratio (nbr) of the
+BOBA CSR (line sizes 32 and 4) and of the direct CSR (32) when it has edges.
 """
 
 import os
@@ -66,6 +68,9 @@ def run_ref(g: CooGraph, x=None):
     out["pr_iters"] = np.array([it])
     sd = boba.sort_coo_by_destination(g)
     out["I_sd"], out["J_sd"] = sd.I, sd.J
+    if g.m:  # §8f f4: neighbourhood line ratio (metrics.py:90-115), BOBA CSR at 32 and 4, direct CSR at 32
+        from boba.metrics import nbr
+        out["nbr"] = np.array([nbr(csr, 32), nbr(csr, 4), nbr(raw, 32)])
     if g.weights is not None:
         out["w2"] = csr.weights
         out["w2_raw"] = raw.weights

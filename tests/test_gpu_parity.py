@@ -63,6 +63,13 @@ def run_case(bb, c):
     assert np.array_equal(sd.I, c["I_sd"]) and np.array_equal(sd.J, c["J_sd"]), "sort_coo_by_destination"
     if c["w"] is not None:
         assert np.array_equal(sd.weights, c["w_sd"])
+    # §8f f4: neighbourhood line ratio on the GPU (fp64 mean; summation order differs from numpy)
+    if g.m:
+        got = [bb.nbr(csr, 32), bb.nbr(csr, 4), bb.nbr(raw, 32)]
+        np.testing.assert_allclose(got, c["nbr"], rtol=1e-12, atol=0)
+    else:
+        with pytest.raises(bb.UndefinedMetricError):
+            bb.nbr(csr)
 
 
 def test_known_answers(bb, kat):

@@ -55,6 +55,9 @@ def check_case(c):
     assert np.array_equal(Is, c["I_sd"]) and np.array_equal(Js, c["J_sd"])
     if c["w"] is not None:
         assert np.array_equal(ws, c["w_sd"])
+    if I.size:  # §8f f4: neighbourhood line ratio
+        got = [oracle.nbr(off, idx, 32), oracle.nbr(off, idx, 4), oracle.nbr(off0, idx0, 32)]
+        np.testing.assert_allclose(got, c["nbr"], rtol=1e-15, atol=0)
 
 
 def test_known_answers(kat):
