@@ -142,7 +142,8 @@ int boba_reorder_to_csr_timed(const uint32_t *I, const uint32_t *J, const double
                               double *weights_out, void *workspace, size_t workspace_bytes,
                               void *stream, void *const *events);
 
-/* --- Captured pipeline (CUDA graph) -------------------------------------
+/* --- Captured pipeline (CUDA graph; the reference's reorder + convert
+ * phases, bench.py:135-149, replayed with one launch) ----------------------
  * Records one boba_reorder_to_csr call on these fixed device buffers (after
  * one eager run, which also produces outputs) into a CUDA graph; each
  * boba_graph_launch replays the whole pipeline with a single launch.  The
@@ -214,7 +215,8 @@ int boba_offset_ids(const uint32_t *in, uint64_t count, uint32_t delta, uint32_t
 /* Compaction of a merged first[] (2 m_global positions) and relabel of a
  * local edge shard (m edges) with the hub label table the compaction builds
  * -- phases 2 and 3 of the multi-GPU pipeline (sharded.py), as in the fused
- * single-GPU call. */
+ * single-GPU call.  Replaces _parallel.compact_ranks (_parallel.py:178-201)
+ * + graph.apply_permutation (graph.py:280-289) on one shard. */
 size_t boba_compact_relabel_workspace_size(uint64_t m_global, uint32_t n);
 int boba_compact_relabel(const uint32_t *first, uint64_t m_global, uint32_t n, const uint32_t *I,
                          const uint32_t *J, uint64_t m, uint32_t *order, uint32_t *label, uint32_t *I2,
