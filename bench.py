@@ -173,11 +173,27 @@ def run_reference(args):
     import oracle
 
     cores = len(os.sched_getaffinity(0))
-    n, m = graph_size(args.config)
-    n, I, J = host_graph(args.config)
-    # bound the run: each step is the full graph when K <= 12, else a prefix
-    # of the edge stream (same n) sized so K steps stay within a few minutes
-    step_m = m if args.steps <= 12 else max(1 << 20, int(m * 12 / args.steps))
+    world = max(int(os.environ.get("WORLD_SIZE", "1")), args.gpus)
+    kind, p, desc = CONFIGS[args.config]
+    workload = desc + ", randomly relabelled"
+    if world > 1 and kind == "rmat":
+        # the GPU arm's weak-scaled graph (scale + log2 N); each step times a
+        # prefix of its edge stream of one GPU's share (the config's m)
+        import math
+
+        scale = p["scale"] + int(round(math.log2(world)))
+        n, m = 1 << scale, p["ef"] << scale
+        step_m = p["ef"] << p["scale"]
+        I, J = oracle.rmat_edges(scale, p["ef"], GEN_SEED, 0, step_m)
+        lab = oracle.random_labels(n, LABEL_SEED)
+        I, J = lab[I], lab[J]
+        workload = f"R-MAT scale {scale} edge factor {p['ef']}, randomly relabelled (weak scaling from {desc})"
+    else:
+        n, m = graph_size(args.config)
+        n, I, J = host_graph(args.config)
+        # bound the run: each step is the full graph when K <= 12, else a prefix
+        # of the edge stream (same n) sized so K steps stay within a few minutes
+        step_m = m if args.steps <= 12 else max(1 << 20, int(m * 12 / args.steps))
     Is, Js = I[:step_m], J[:step_m]
     for _ in range(min(args.warmup, 1)):
         cpu_pipeline_time(n, Is, Js, cores)
@@ -198,7 +214,7 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "int64",
         "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config][2] + ", randomly relabelled", "n": n, "m": m},
+        "config": {"workload": workload, "n": n, "m": m},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 5), "unit": "GEdges/s", "cores": cores, "kind": "port",
                          "sample": sample,
