@@ -1,6 +1,6 @@
 // Reference point only (not product code): time CUB's onesweep radix sort of
 // 67M (uint32 key, uint32 value) pairs over 22 key bits, as a target for the
-// hand-written stable pass in csrc/onesweep.cuh.
+// hand-written stable passes in csrc/radix.cuh.
 #include <cub/cub.cuh>
 #include <cstdio>
 #include <cstdint>
