@@ -5,16 +5,19 @@
 // ascending ID order) and graph.py:205-208 (label[order[k]] = k).
 //
 // B200 formulation (three kernels, all O(n) random or O(m/32) streaming):
-//   k_mark          one bit per used position: atomicOr into a 2m-bit map.
-//   k_sector_scan   single-pass decoupled-lookback exclusive scan of the
-//                   popcount of every 256-bit sector -> secprefix[]; the
+//   k_mark          one bit per used position: atomicOr into a 2m-bit map
+//                   stored as 32-byte records of 224 bits (7 words) plus, in
+//                   the record's 8th word, the number of set bits before it.
+//   k_rec_scan      single-pass decoupled-lookback exclusive scan of the
+//                   records' popcounts, written into their 8th words; the
 //                   total is n_seen (vertices that occur at all).
-//   k_assign        per vertex: rank = secprefix[sector] + popcount of the
-//                   bits below it inside its (one 32-byte) sector, or, for a
-//                   vertex that never occurs, n_seen + its rank among the
-//                   isolated vertices (a second lookback scan over vertex
-//                   tiles keeps them in ascending ID order).  Writes
-//                   label[v] = rank (coalesced) and order[rank] = v.
+//   k_assign        per vertex: rank = record prefix + popcount of the bits
+//                   below it in its record -- one 32-byte sector, so one
+//                   random access per vertex -- or, for a vertex that never
+//                   occurs, n_seen + its rank among the isolated vertices (a
+//                   second lookback scan over vertex tiles keeps them in
+//                   ascending ID order).  Writes label[v] = rank (coalesced)
+//                   and order[rank] = v.
 // No gather of I||J is needed: position first[v] holds v by definition.
 #include "common.cuh"
 #include "hubs.cuh"
@@ -23,38 +26,44 @@
 namespace boba {
 
 constexpr int kScanNT = 256;
-constexpr int kSectorsPerThread = 4;                    // 4 x 32 B per thread
-constexpr int kSectorsPerTile = kScanNT * kSectorsPerThread;
+constexpr int kRecWords = 7;                            // bitmap words per 32-byte record
+constexpr uint32_t kRecBits = 32 * kRecWords;           // 224 positions per record
+constexpr int kRecsPerThread = 4;
+constexpr int kRecsPerTile = kScanNT * kRecsPerThread;
 constexpr int kAssignVPT = 4;                           // vertices per thread
 constexpr int kAssignTile = kScanNT * kAssignVPT;
 
-__global__ void k_mark(const uint32_t* __restrict__ first, uint32_t n, uint32_t* bits) {
+// word w of the bitmap (position p: w = p >> 5) -> its index in the record array
+__device__ __forceinline__ uint32_t rec_of_word(uint32_t w) { return w / kRecWords; }
+
+__global__ void k_mark(const uint32_t* __restrict__ first, uint32_t n, uint32_t* recs) {
     uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-        uint32_t f = __ldg(first + v);
-        if (f != BOBA_UNSET) atomicOr(bits + (f >> 5), 1u << (f & 31));
+        const uint32_t f = __ldg(first + v);
+        if (f != BOBA_UNSET) {
+            const uint32_t w = f >> 5, r = rec_of_word(w);
+            atomicOr(recs + 8 * r + (w - r * kRecWords), 1u << (f & 31));
+        }
     }
 }
 
-__global__ void __launch_bounds__(kScanNT) k_sector_scan(const uint4* __restrict__ bits, uint64_t sectors,
-                                                         uint32_t* secprefix, unsigned long long* status,
-                                                         unsigned* tile_counter, uint32_t* n_seen) {
+__global__ void __launch_bounds__(kScanNT) k_rec_scan(uint4* recs, uint64_t nrec, unsigned long long* status,
+                                                      unsigned* tile_counter, uint32_t* n_seen) {
     __shared__ unsigned s_tile;
     __shared__ uint32_t s_scan[kScanNT / 32 + 1];
     __shared__ unsigned long long s_excl;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const uint64_t tile = s_tile;
-    const uint64_t s0 = tile * kSectorsPerTile + (uint64_t)threadIdx.x * kSectorsPerThread;
-    uint32_t cnt[kSectorsPerThread];
+    const uint64_t r0 = tile * kRecsPerTile + (uint64_t)threadIdx.x * kRecsPerThread;
+    uint32_t cnt[kRecsPerThread];
     uint32_t sum = 0;
 #pragma unroll
-    for (int k = 0; k < kSectorsPerThread; k++) {
+    for (int k = 0; k < kRecsPerThread; k++) {
         uint32_t c = 0;
-        if (s0 + k < sectors) {
-            uint4 a = bits[2 * (s0 + k)], b = bits[2 * (s0 + k) + 1];
-            c = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) +
-                __popc(b.z) + __popc(b.w);
+        if (r0 + k < nrec) {
+            const uint4 a = recs[2 * (r0 + k)], b = recs[2 * (r0 + k) + 1];
+            c = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) + __popc(b.z);
         }
         cnt[k] = c;
         sum += c;
@@ -68,36 +77,34 @@ __global__ void __launch_bounds__(kScanNT) k_sector_scan(const uint4* __restrict
         if (threadIdx.x == 0) {
             if (tile != 0) st_volatile_u64(status + tile, kFlagInc | (ex + total));
             s_excl = ex;
-            uint64_t ntiles = ceil_div(sectors, kSectorsPerTile);
-            if (tile == ntiles - 1) *n_seen = (uint32_t)(ex + total);
+            if (tile == ceil_div(nrec, kRecsPerTile) - 1) *n_seen = (uint32_t)(ex + total);
         }
     }
     __syncthreads();
     uint32_t run = (uint32_t)s_excl + excl_thread;
+    uint32_t* words = reinterpret_cast<uint32_t*>(recs);
 #pragma unroll
-    for (int k = 0; k < kSectorsPerThread; k++) {
-        if (s0 + k < sectors) secprefix[s0 + k] = run;
+    for (int k = 0; k < kRecsPerThread; k++) {
+        if (r0 + k < nrec) words[8 * (r0 + k) + kRecWords] = run;
         run += cnt[k];
     }
 }
 
-__device__ __forceinline__ uint32_t rank_of(uint32_t f, const uint4* __restrict__ bits,
-                                            const uint32_t* __restrict__ secprefix) {
-    const uint32_t s = f >> 8, w = (f >> 5) & 7, b = f & 31;
-    uint4 lo = __ldg(bits + 2 * s), hi = __ldg(bits + 2 * s + 1);
-    uint32_t words[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-    uint32_t r = __ldg(secprefix + s);
+__device__ __forceinline__ uint32_t rank_of(uint32_t f, const uint4* __restrict__ recs) {
+    const uint32_t w = f >> 5, r = rec_of_word(w), wi = w - r * kRecWords, b = f & 31;
+    const uint4 lo = __ldg(recs + 2 * r), hi = __ldg(recs + 2 * r + 1);
+    const uint32_t words[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t rank = words[kRecWords];
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-        if ((uint32_t)k < w) r += __popc(words[k]);
-        else if ((uint32_t)k == w) r += __popc(words[k] & ((1u << b) - 1u));
+    for (int k = 0; k < kRecWords; k++) {
+        if ((uint32_t)k < wi) rank += __popc(words[k]);
+        else if ((uint32_t)k == wi) rank += __popc(words[k] & ((1u << b) - 1u));
     }
-    return r;
+    return rank;
 }
 
 __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__ first, uint32_t n,
-                                                    const uint4* __restrict__ bits,
-                                                    const uint32_t* __restrict__ secprefix,
+                                                    const uint4* __restrict__ recs,
                                                     const uint32_t* __restrict__ n_seen_ptr,
                                                     uint32_t* order, uint32_t* label,
                                                     unsigned long long* status, unsigned* tile_counter) {
@@ -132,7 +139,7 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
 #pragma unroll
     for (int k = 0; k < kAssignVPT; k++) {
         if (v0 + k >= n) continue;
-        uint32_t r = (f[k] == BOBA_UNSET) ? iso_rank++ : rank_of(f[k], bits, secprefix);
+        uint32_t r = (f[k] == BOBA_UNSET) ? iso_rank++ : rank_of(f[k], recs);
         lab[k] = r;
         order[r] = (uint32_t)(v0 + k);
     }
@@ -161,16 +168,16 @@ __global__ void k_hub_labels(const uint32_t* __restrict__ order, uint32_t K, Hub
 
 namespace {
 struct CompactWs {
-    uint32_t* bits;
-    uint32_t* secprefix;
-    unsigned long long* st_sec;
+    uint32_t* recs;     // 2m-bit map in 32-byte records (7 words + prefix)
+    unsigned long long* st_rec;
     unsigned long long* st_v;
     unsigned* counters;
     size_t total;
 };
+uint64_t num_recs(uint64_t m) { return ceil_div(2 * m + 1, kRecBits) + 1; }
 CompactWs carve_compact(void* base, uint64_t m, uint32_t n) {
-    const uint64_t sectors = ceil_div(2 * m, 256) + 1;
-    const uint64_t sec_tiles = ceil_div(sectors, kSectorsPerTile);
+    const uint64_t nrec = num_recs(m);
+    const uint64_t rec_tiles = ceil_div(nrec, kRecsPerTile);
     const uint64_t v_tiles = ceil_div((uint64_t)n, kAssignTile) + 1;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -179,12 +186,11 @@ CompactWs carve_compact(void* base, uint64_t m, uint32_t n) {
         return base ? static_cast<char*>(base) + o : nullptr;
     };
     CompactWs w;
-    w.bits = (uint32_t*)take(sectors * 32);
-    w.st_sec = (unsigned long long*)take(sec_tiles * 8);
+    w.recs = (uint32_t*)take(nrec * 32);
+    w.st_rec = (unsigned long long*)take(rec_tiles * 8);
     w.st_v = (unsigned long long*)take(v_tiles * 8);
     w.counters = (unsigned*)take(64);
-    w.secprefix = (uint32_t*)take(sectors * 4);  // last: not cleared
-    w.total = off;
+    w.total = off;  // all of it is cleared per call
     return w;
 }
 }  // namespace
@@ -196,26 +202,24 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
                            size_t ws_bytes, int num_sms, cudaStream_t s) {
     if (ws_bytes < compact_workspace_bytes(m, n)) return cudaErrorInvalidValue;
     if (n == 0) return cudaSuccess;
-    const uint64_t sectors = ceil_div(2 * m, 256) + 1;
-    const uint64_t sec_tiles = ceil_div(sectors, kSectorsPerTile);
+    const uint64_t nrec = num_recs(m);
+    const uint64_t rec_tiles = ceil_div(nrec, kRecsPerTile);
     const uint64_t v_tiles = ceil_div((uint64_t)n, kAssignTile);
     CompactWs w = carve_compact(ws, m, n);
-    uint32_t* bits = w.bits;
-    uint32_t* secprefix = w.secprefix;
     unsigned* counters = w.counters;
     uint32_t* n_seen = counters + 4;
-    // clear bits, lookback status and counters (everything before secprefix)
-    cudaError_t err = cudaMemsetAsync(ws, 0, reinterpret_cast<char*>(secprefix) - static_cast<char*>(ws), s);
+    // clear the records (bits and prefixes), lookback status and counters
+    cudaError_t err = cudaMemsetAsync(ws, 0, w.total, s);
     if (err != cudaSuccess) return err;
     {
         uint64_t blocks = ceil_div(n, 256);
         uint64_t cap = (uint64_t)num_sms * 16;
-        k_mark<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(first, n, bits);
+        k_mark<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(first, n, w.recs);
     }
-    k_sector_scan<<<(int)sec_tiles, kScanNT, 0, s>>>(reinterpret_cast<const uint4*>(bits), sectors,
-                                                     secprefix, w.st_sec, counters + 0, n_seen);
-    k_assign<<<(int)v_tiles, kScanNT, 0, s>>>(first, n, reinterpret_cast<const uint4*>(bits), secprefix,
-                                              n_seen, order, label, w.st_v, counters + 1);
+    k_rec_scan<<<(int)rec_tiles, kScanNT, 0, s>>>(reinterpret_cast<uint4*>(w.recs), nrec, w.st_rec, counters + 0,
+                                                  n_seen);
+    k_assign<<<(int)v_tiles, kScanNT, 0, s>>>(first, n, reinterpret_cast<const uint4*>(w.recs), n_seen, order, label,
+                                              w.st_v, counters + 1);
     if (n_seen_out) cudaMemcpyAsync(n_seen_out, n_seen, 4, cudaMemcpyDeviceToDevice, s);
     if (hubs) {
         // HubLabels (hubs.cuh) for phase 3: labels [0, kHubMaxLabel), kHubWays
