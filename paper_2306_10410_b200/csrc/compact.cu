@@ -152,18 +152,23 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
     }
 }
 
-// table = kHubWays arrays of kHubBuckets entries; round r fills way r with the
-// smallest label that did not win an earlier way of its bucket.
-__global__ void k_hub_labels(const uint32_t* __restrict__ order, uint32_t K, HubHash hh, int round,
-                             uint32_t* table) {
+// table = kHubWays arrays of kHubBuckets entries holding, per bucket, the
+// kHubWays smallest entries (label << tag_bits | tag) in ascending order, in
+// one pass: an entry goes through the ways with atomicMin and carries the
+// larger of itself and the displaced value on to the next way, so every value
+// but a way's final minimum reaches the next way exactly once.
+__global__ void k_hub_labels(const uint32_t* __restrict__ order, uint32_t K, HubHash hh, uint32_t* table) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= K) return;
     uint32_t b, tag;
     hh.split(__ldg(order + k), b, tag);
-    const uint32_t e = (k << hh.tag_bits) | tag;
-    for (int w = 0; w < round; w++)
-        if (table[w * kHubBuckets + b] == e) return;
-    atomicMin(table + round * kHubBuckets + b, e);
+    uint32_t e = (k << hh.tag_bits) | tag;
+#pragma unroll
+    for (int w = 0; w < kHubWays; w++) {
+        const uint32_t old = atomicMin(table + w * kHubBuckets + b, e);
+        e = old > e ? old : e;
+        if (e == 0xFFFFFFFFu) break;  // filled an empty slot: nothing to carry
+    }
 }
 
 namespace {
@@ -223,15 +228,13 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
     if (n_seen_out) cudaMemcpyAsync(n_seen_out, n_seen, 4, cudaMemcpyDeviceToDevice, s);
     if (hubs) {
         // HubLabels (hubs.cuh) for phase 3: labels [0, kHubMaxLabel), kHubWays
-        // slots per bucket, smaller labels first (one round per slot).
+        // slots per bucket, the smallest labels of each bucket (one pass).
         const HubHash hh = HubHash::make(n);
         if (hh.tag_bits <= 16) {
             err = cudaMemsetAsync(hubs, 0xFF, kHubTableBytes, s);
             if (err != cudaSuccess) return err;
             const uint32_t K = n < kHubMaxLabel ? n : kHubMaxLabel;
-            for (int round = 0; round < kHubWays; round++)
-                k_hub_labels<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(order, K, hh, round,
-                                                                       reinterpret_cast<uint32_t*>(hubs));
+            k_hub_labels<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(order, K, hh, reinterpret_cast<uint32_t*>(hubs));
         } else {
             err = cudaMemsetAsync(hubs, 0xFF, kHubTableBytes, s);  // empty table: relabel gathers everything
             if (err != cudaSuccess) return err;
