@@ -670,14 +670,14 @@ def csr_passes(n):
 
 def launches_per_step(m, n):
     """Kernels boba_reorder_to_csr launches (csrc/api.cu): first occurrence
-    (two-stage: prefix sweep, SeenSet build, main sweep; + scalar tail),
-    mark/sector-scan/assign + 3 hub-table rounds, relabel (+ scalar tail),
+    (two-stage: prefix pass, SeenSet build, main sweep; + scalar tail),
+    mark/record-scan/assign + the hub-table build, relabel (+ scalar tail),
     the offsets[n] store, per radix pass upsweep/scan/downsweep, suffix-min."""
     tail = 1 if m % 4 else 0
     kk = max((n - 1).bit_length() if n > 1 else 0, 14)
     prefix = 131072 if kk - 14 <= 8 else 65536
     first_hit = (3 if (kk - 14 <= 16 and m >= 16 * prefix) else 1) + tail
-    compact = 3 + (3 if kk - 14 <= 16 else 0)
+    compact = 3 + (1 if kk - 14 <= 16 else 0)
     return first_hit + compact + (1 + tail) + 1 + 3 * csr_passes(n) + 1
 
 
