@@ -109,6 +109,39 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ 
     }
 }
 
+// label[] beyond L2 (s26: 268 MB): gathers over the whole table miss L2 and cost
+// a DRAM sector each.  Instead the id space is cut into ranges whose slice of
+// label[] stays L2-resident, and the edge streams are passed once per range.
+// Pass 0 reads I, J and writes label[v] for v in its range, v | kRlFlag for the
+// rest; later passes rewrite I2, J2 in place, resolving the flagged ids in
+// their range (n <= 2^31, so the flag bit is free).
+constexpr uint32_t kRlFlag = 0x80000000u;
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kRlNT, 1) k_relabel_range(const uint4* __restrict__ I, const uint4* __restrict__ J,
+                                                            uint64_t quads, const uint32_t* __restrict__ label,
+                                                            uint32_t lo, uint32_t width, uint4* I2, uint4* J2) {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    auto fix = [&](uint32_t v) -> uint32_t {
+        const uint32_t id = FIRST ? v : v ^ kRlFlag;
+        if (!FIRST && !(v & kRlFlag)) return v;
+        if (id - lo < width) return ld_label(label + id, true, pol);
+        return id | kRlFlag;
+    };
+    for (uint64_t t = blockIdx.x; t * kRlNT < quads; t += gridDim.x) {
+        const uint64_t q = t * kRlNT + threadIdx.x;
+        if (q < quads) {
+            const uint4 a = FIRST ? __ldcs(I + q) : __ldcs(I2 + q), b = FIRST ? __ldcs(J + q) : __ldcs(J2 + q);
+            uint4 ra, rb;
+            ra.x = fix(a.x); ra.y = fix(a.y); ra.z = fix(a.z); ra.w = fix(a.w);
+            rb.x = fix(b.x); rb.y = fix(b.y); rb.z = fix(b.z); rb.w = fix(b.w);
+            __stcs(I2 + q, ra);
+            __stcs(J2 + q, rb);
+        }
+    }
+}
+
 template <bool HIST>
 __global__ void k_relabel_scalar(const uint32_t* __restrict__ I, const uint32_t* __restrict__ J,
                                  uint64_t e0, uint64_t m, const uint32_t* __restrict__ label,
@@ -161,9 +194,26 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
             if (hubs) launch_vec<1, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
             else launch_vec<1, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
         } else if (n > (1u << 24)) {
-            // measured at s26: 22.6 -> 21.8 ms (with the hub table in shared memory instead: 25.1 ms --
-            // it leaves the L1, which holds the hot labels here, only ~36 KB)
-            launch_vec<0, false, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
+            // single pass, measured at s26: 22.6 -> 21.8 ms (with the hub table in shared memory
+            // instead: 25.1 ms -- it leaves the L1, which holds the hot labels here, only ~36 KB)
+            // range passes keep each slice of label[] <= 128 MiB (measured at s26:
+            // 1 pass 21.9 ms, 2 passes 14.1, 3 passes 14.3, 4 passes 16.7)
+            const char* e = getenv("BOBA_RL_PASSES");
+            const uint32_t passes = e ? (uint32_t)atoi(e) : (uint32_t)ceil_div(n, 1u << 25);
+            if (passes <= 1 || n > kRlFlag) {
+                launch_vec<0, false, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
+            } else {
+                const uint32_t width = (uint32_t)ceil_div(n, passes);
+                for (uint32_t p = 0; p < passes; p++) {
+                    const uint32_t lo = p * width;
+                    if (p == 0)
+                        k_relabel_range<true><<<grid, kRlNT, 0, s>>>((const uint4*)I, (const uint4*)J, quads, label,
+                                                                     lo, width, (uint4*)I2, (uint4*)J2);
+                    else
+                        k_relabel_range<false><<<grid, kRlNT, 0, s>>>((const uint4*)I2, (const uint4*)J2, quads,
+                                                                      label, lo, width, (uint4*)I2, (uint4*)J2);
+                }
+            }
         } else {
             if (hubs) launch_vec<0, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
             else launch_vec<0, false>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);

@@ -307,12 +307,17 @@ def test_host_pipeline_matches_device(dev):
     hp.close()
 
 
-def test_first_occurrence_waves_beyond_l2(dev):
+@pytest.mark.parametrize("relabel_passes", [None, "3"])
+def test_first_occurrence_waves_beyond_l2(dev, monkeypatch, relabel_passes):
     """n > 2^24: the fused pipeline's first-occurrence sweep guards on a
     seen-bitmap in waves of 2^26 positions (first[] no longer fits in L2).
     m = 2^26 edges -> 2^27 positions, two waves; the whole pipeline is
-    checked against the oracle."""
+    checked against the oracle.  With BOBA_RL_PASSES the relabel runs as
+    range passes (the default beyond n = 2^25) over the same graph."""
     import torch
+
+    if relabel_passes:
+        monkeypatch.setenv("BOBA_RL_PASSES", relabel_passes)
 
     scale = 25
     n = 1 << scale
