@@ -327,6 +327,23 @@ def test_first_occurrence_waves_beyond_l2(dev, monkeypatch, relabel_passes):
     pipeline_vs_oracle(dev, I, J, n)
 
 
+def test_relabel_range_passes_ragged(dev):
+    """n = 2^25 + 5: the relabel runs as two range passes by default (label[]
+    beyond 128 MiB) with a ragged split, and m = 3 mod 4 leaves a scalar tail;
+    ids on both sides of the split and at the ends are present."""
+    import torch
+
+    n, m = (1 << 25) + 5, 3 * (1 << 20) + 3
+    width = -(-n // 2)
+    rng = np.random.default_rng(17)
+    I = rng.integers(0, n, m, dtype=np.int64)
+    J = rng.integers(0, n, m, dtype=np.int64)
+    edge = np.array([0, width - 1, width, width + 1, n - 1, n - 2], dtype=np.int64)
+    I[: edge.size], J[m - edge.size:] = edge, edge[::-1]
+    t = lambda a: torch.from_numpy(a.astype(np.uint32).view(np.int32)).cuda()  # noqa: E731
+    pipeline_vs_oracle(dev, t(I), t(J), n)
+
+
 def test_captured_pipeline_replays_new_inputs(dev):
     """boba_reorder_to_csr_graph_create: the captured step reproduces the
     direct call, and replaying it after new edges are copied into the same
