@@ -583,14 +583,19 @@ def run_sharded(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # --share-gpu: every rank on cuda:0 over gloo -- a functional run of the N > 1
+    # flow on a one-GPU box (NCCL refuses two ranks per device); not a measurement
+    local = 0 if args.share_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if not dist.is_initialized():
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29511")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+        if args.share_gpu:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     kind, p, desc = CONFIGS[args.config]
     if kind != "rmat":
         raise SystemExit("the sharded path runs the R-MAT configs")
@@ -690,6 +695,8 @@ def run_sharded(args):
                                       + 3 * csr_passes(max(res.row_hi - res.row_lo, 1)) + 2),
         "clocks": clk.summary(),
     }
+    if args.share_gpu:
+        line["share_gpu"] = "ranks share cuda:0 over gloo: functional run of the N > 1 flow, not a measurement"
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -723,6 +730,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-spmv-c3", action="store_true", help="skip the c3 (grid, 100 SpMV) e2e comparison")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded pipeline even on 1 GPU")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="(debug) all torchrun ranks on cuda:0 over gloo: runs the N > 1 flow on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
