@@ -9,7 +9,7 @@
 //
 // Merge-path, perfectly balanced over the n + m "merge items" (row ends and
 // nonzeros), so hub rows of skewed graphs cost the same as short rows:
-//   * each CTA owns 2048 consecutive merge items; it locates its (row, nnz)
+//   * each CTA owns 1024 consecutive merge items; it locates its (row, nnz)
 //     start with a binary search on the row-end offsets, stages the row ends
 //     and the products x[indices[k]]*w[k] in shared memory with coalesced
 //     index loads (the x gathers are all in flight at once -- this is where
@@ -27,7 +27,10 @@
 
 namespace boba {
 
-constexpr int kSpNT = 256, kSpIPT = 8, kSpTile = kSpNT * kSpIPT;
+// 128 x 8: measured against 256 x 8 / 512 x 8 / 256 x 16 / 256 x 4 / 64 x 8 / 128 x 16
+// (c3 BOBA SpMV 0.219 vs 0.227 / 0.238 / 0.309 / 0.248 / 0.226 / 0.281 ms): smaller
+// CTAs lose less to the two block barriers of this latency-bound tile.
+constexpr int kSpNT = 128, kSpIPT = 8, kSpTile = kSpNT * kSpIPT;
 constexpr int kSpShort = 8;  // longest in-tile row the per-row fold takes (longer: divergent folds)
 
 // Streaming loads that must not evict the x vector's hot lines from L1.
