@@ -40,6 +40,14 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
     return v;
 }
 
+__device__ __forceinline__ uint4 ld_stream_u128(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 template <typename T>
 struct SegValT {
     bool f;
@@ -99,7 +107,7 @@ __device__ __forceinline__ uint32_t merge_search_rel(const uint32_t* a, uint32_t
 // Inside the tile all indices are 32-bit and relative to the tile's first
 // row (i0) and first nonzero (j0); only the global loads and stores use
 // 64-bit addresses.
-template <typename T>
+template <typename T, bool VEC>
 __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restrict__ offsets,
                                           const uint32_t* __restrict__ indices, const T* __restrict__ w,
                                           const T* __restrict__ x, T* __restrict__ y, uint32_t n, uint64_t m,
@@ -116,7 +124,49 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restr
     const uint32_t j0_32 = (uint32_t)j0;  // offsets are uint32: relative ends are exact mod 2^32
     for (uint32_t k = gt; k <= nrows; k += kSpNT)
         s_end[k] = (i0 + k < n) ? ld_stream_u32(offsets + i0 + 1 + k) - j0_32 : 0xFFFFFFFFu;
-    {
+    // VEC (fp32, unweighted, 16-byte aligned indices): the tile's indices are
+    // read as aligned quads from a0 = j0 & ~3 and the products stored as
+    // quads at their a0-relative slot, so s_val[k + sh] holds item k
+    const uint32_t sh = VEC ? (uint32_t)(j0 & 3) : 0u;
+    if (VEC) {
+        const uint64_t a0 = j0 - sh;
+        const uint32_t span = nnz + sh, quads = (span + 3) >> 2;
+        const uint4* ip4 = reinterpret_cast<const uint4*>(indices + a0);
+        constexpr int QPT = kSpIPT / 4 + 1;  // span <= kSpTile + 3: one quad beyond kSpTile / 4
+        uint4 c[QPT];
+#pragma unroll
+        for (int u = 0; u < QPT; u++) {
+            const uint32_t q = gt + u * kSpNT;
+            c[u] = make_uint4(0, 0, 0, 0);
+            if (q < quads) {
+                if (a0 + 4ull * q + 4 <= m) {
+                    c[u] = ld_stream_u128(ip4 + q);
+                } else {  // the array's last partial quad: no read past indices[m)
+                    const uint32_t* ip = indices + a0 + 4ull * q;
+                    const uint64_t left = m - (a0 + 4ull * q);
+                    c[u].x = ld_stream_u32(ip);
+                    if (left > 1) c[u].y = ld_stream_u32(ip + 1);
+                    if (left > 2) c[u].z = ld_stream_u32(ip + 2);
+                }
+            }
+        }
+        // every gather in flight before the first store (the random case is miss-bound)
+        const float* xf = reinterpret_cast<const float*>(x);
+        float4 v[QPT];
+#pragma unroll
+        for (int u = 0; u < QPT; u++) {
+            const uint32_t r = 4 * (gt + u * kSpNT);
+            v[u].x = r + 0 >= sh && r + 0 < span ? __ldg(xf + c[u].x) : 0.f;
+            v[u].y = r + 1 >= sh && r + 1 < span ? __ldg(xf + c[u].y) : 0.f;
+            v[u].z = r + 2 >= sh && r + 2 < span ? __ldg(xf + c[u].z) : 0.f;
+            v[u].w = r + 3 >= sh && r + 3 < span ? __ldg(xf + c[u].w) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < QPT; u++) {
+            const uint32_t q = gt + u * kSpNT;
+            if (q < quads) reinterpret_cast<float4*>(s_val)[q] = v[u];
+        }
+    } else {
         // all index loads, then all x gathers in flight together (nnz <= kSpTile)
         const uint32_t* ip = indices + j0;
         uint32_t col[kSpIPT];
@@ -143,6 +193,7 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restr
     // merge-path fold below.  The choice depends on the matrix only, so y
     // stays bitwise deterministic.
     __syncthreads();
+    const T* sv = s_val + sh;
     // (nnz > (nrows + 1) kSpShort: some row is long by pigeonhole -- skip the check)
     if (nnz <= (nrows + 1) * (uint32_t)kSpShort) {
         bool long_row = false;
@@ -154,12 +205,12 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restr
             for (uint32_t k = gt; k < nrows; k += kSpNT) {
                 const uint32_t beg = k ? s_end[k - 1] : 0u, end = s_end[k];
                 T acc = 0;
-                for (uint32_t j = beg; j < end; j++) acc += s_val[j];
+                for (uint32_t j = beg; j < end; j++) acc += sv[j];
                 y[i0 + k] = acc;  // row 0 may have begun in earlier tiles: k_spmv_carry adds their tails
             }
             if (gt == 0) {
                 T tail = 0;
-                for (uint32_t j = nrows ? s_end[nrows - 1] : 0u; j < nnz; j++) tail += s_val[j];
+                for (uint32_t j = nrows ? s_end[nrows - 1] : 0u; j < nnz; j++) tail += sv[j];
                 tile_tail[tile] = tail;
                 tile_head[tile] = nrows ? i0 : 0xFFFFFFFFu;
             }
@@ -176,7 +227,7 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restr
     bool emitted = false;
     for (uint32_t k = 0; k < items; k++) {
         if (jt < s_end[it]) {
-            acc += s_val[jt];
+            acc += sv[jt];
             jt++;
         } else {
             if (!emitted) {
@@ -235,7 +286,7 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restr
 }
 
 // One merge-path tile per CTA.
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict__ offsets,
                                                       const uint32_t* __restrict__ indices,
                                                       const T* __restrict__ w, const T* __restrict__ x,
@@ -245,9 +296,9 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
                                                       const int* stop) {
     if (stop && *(volatile const int*)stop) return;
     __shared__ uint32_t s_end[kSpTile + 1];
-    __shared__ T s_val[kSpTile];
+    __shared__ __align__(16) T s_val[kSpTile + 4];
     __shared__ SegValT<T> s_warp[kSpNT / 32];
-    spmv_tile<T>(blockIdx.x, offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail, s_end, s_val, s_warp);
+    spmv_tile<T, VEC>(blockIdx.x, offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail, s_end, s_val, s_warp);
 }
 
 // Chunk aggregates of the per-CTA (has_head, tail) pairs: a segmented sum
@@ -372,8 +423,25 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
         k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
     // (A persistent variant with a 128 KB shared-memory copy of the hub prefix of x
     // was measured slower at c2/c3: the occupancy it costs outweighs the hits.)
-    k_spmv_merge<T><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head,
-                                                      tile_tail, stop);
+    const bool vec = sizeof(T) == 4 && !w && (reinterpret_cast<uintptr_t>(indices) & 15) == 0;
+    if (vec) {
+        // Pinned 50 % shared-memory carveout: left to the driver, the vector kernel's
+        // lower register count buys more resident CTAs at the cost of L1, which the
+        // x gathers of poorly ordered graphs depend on (c3 random labels: 0.417 ms
+        // with the default, 0.367 ms pinned; BOBA order: 0.185 / 0.202 ms; the
+        // scalar staging: 0.372 / 0.220 ms).
+        static bool carve = false;
+        if (!carve) {
+            cudaFuncSetAttribute(k_spmv_merge<T, sizeof(T) == 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 50);
+            carve = true;
+        }
+    }
+    if (vec)
+        k_spmv_merge<T, sizeof(T) == 4><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords,
+                                                                          tile_head, tile_tail, stop);
+    else
+        k_spmv_merge<T, false><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head,
+                                                                 tile_tail, stop);
     if (tiles > 1) {
         k_spmv_chunk_agg<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val,
                                                                  stop);

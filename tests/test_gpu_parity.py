@@ -286,6 +286,37 @@ def test_spmv_determinism_and_integer_exactness(dev):
     assert torch.equal(dev.spmv(off, idx, xr), dev.spmv(off, idx, xr))
 
 
+@pytest.mark.parametrize("n,mod", [(1, 1), (37, 2), (5000, 3), (70001, 1), (300000, 0)])
+def test_spmv_vector_staging_edges(dev, n, mod):
+    """fp32 SpMV: the 16-byte staging path (aligned indices) and the scalar
+    one (indices one element off alignment) give bitwise the same y, equal to
+    the oracle on integer data; m = mod (mod 4) leaves a partial last quad;
+    rows mix empty, short and tile-spanning hub rows."""
+    import torch
+
+    rng = np.random.default_rng(n + mod)
+    deg = rng.choice([0, 1, 2, 3, 4, 7], size=n)
+    deg[rng.integers(0, n, max(1, n // 5000))] += rng.integers(1000, 5000)   # hubs across tiles
+    m = int(deg.sum())
+    deg[0] += (mod - m) % 4
+    m = int(deg.sum())
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(deg)
+    idx = rng.integers(0, n, m)
+    x = rng.integers(0, 4, n).astype(np.float32)
+    t_off = torch.from_numpy(off.astype(np.uint32).view(np.int32)).cuda()
+    aligned = torch.from_numpy(idx.astype(np.uint32).view(np.int32)).cuda()
+    buf = torch.empty(m + 1, dtype=torch.int32, device="cuda")
+    buf[1:] = aligned
+    shifted = buf[1:]                                     # 4 bytes past a 16-byte boundary
+    xs = torch.from_numpy(x).cuda()
+    y_vec = dev.spmv(t_off, aligned, xs)
+    y_sca = dev.spmv(t_off, shifted, xs)
+    assert torch.equal(y_vec, y_sca)
+    want = oracle.spmv_pull(off, idx, x.astype(np.float64))
+    assert np.array_equal(y_vec.cpu().numpy().astype(np.float64), want)
+
+
 def test_host_pipeline_matches_device(dev):
     import torch
 
