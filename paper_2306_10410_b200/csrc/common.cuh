@@ -3,6 +3,7 @@
 // single-pass scan in the library (sector ranks, isolated-vertex ranks, CSR
 // offsets, radix bucket offsets and the SpMV row carries).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -138,5 +139,25 @@ __device__ __forceinline__ unsigned long long warp_lookback_min(const unsigned l
 }
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Kernel attributes (dynamic shared memory limit, carveout) belong to the
+// device's context: a call site sets them once per device, tracked here.
+struct PerDeviceOnce {
+    std::atomic<unsigned long long> done{0};
+    // true the first time it is asked on the current device (devices >= 64 always ask)
+    bool first() {
+        int d = 0;
+        cudaGetDevice(&d);
+        if (d >= 64) return true;
+        const unsigned long long bit = 1ull << d;
+        return !(done.fetch_or(bit) & bit);
+    }
+};
+
+template <typename K>
+inline cudaError_t set_attr_once(PerDeviceOnce& once, K* kernel, cudaFuncAttribute a, int v) {
+    if (!once.first()) return cudaSuccess;
+    return cudaFuncSetAttribute(kernel, a, v);
+}
 
 }  // namespace boba

@@ -274,13 +274,10 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
                           unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
                           int num_sms, cudaStream_t s, uint32_t* row_starts = nullptr) {
     using C = RadixCfg<RB, NT, IPT>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_radix_downsweep<RB, NT, IPT, MINB, Op>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static PerDeviceOnce attr;
+    if (cudaError_t e = set_attr_once(attr, k_radix_downsweep<RB, NT, IPT, MINB, Op>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM))
+        return e;
     const uint64_t tiles = ceil_div(m, C::TILE);
     const uint64_t hcount = tiles << bits;
     const uint64_t up_grid = tiles < (uint64_t)num_sms * 8 ? tiles : (uint64_t)num_sms * 8;

@@ -212,11 +212,8 @@ template <int TW, bool BITS = false>
 static void launch_static(const Ranges& r, uint32_t* first, const unsigned long long* seen_g, const HubHash& hh,
                           int num_sms, cudaStream_t s, const uint32_t* seenb = nullptr, uint32_t* newb = nullptr) {
     const size_t smem = sizeof(unsigned long long) * kHubBuckets;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_first_hit_static<TW, BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    set_attr_once(attr, k_first_hit_static<TW, BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_first_hit_static<TW, BITS><<<num_sms, kFhNT, smem, s>>>(r, first, seen_g, hh, seenb, newb);
 }
 
@@ -290,11 +287,8 @@ __global__ void k_first_hit_scalar(const uint32_t* __restrict__ I, const uint32_
 template <bool RELAXED>
 static void launch_sweep(const Ranges& r, uint32_t* first, int num_sms, cudaStream_t s) {
     const size_t smem = sizeof(uint32_t) << kFhSlotsLog2;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_first_hit<RELAXED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    set_attr_once(attr, k_first_hit<RELAXED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const uint64_t iters = ceil_div(r.qa + r.qb, (uint64_t)kFhNT * kFhQuads);
     if (iters == 0) return;
     const int grid = (int)(iters < (uint64_t)num_sms ? iters : (uint64_t)num_sms);

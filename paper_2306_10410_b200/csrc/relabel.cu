@@ -159,11 +159,8 @@ template <int MODE, bool HUBS, bool STREAM = false>
 static void launch_vec(int grid, size_t smem, cudaStream_t s, const uint32_t* I, const uint32_t* J, uint64_t quads,
                        const uint32_t* label, const unsigned long long* hubs, uint32_t n, uint32_t* I2, uint32_t* J2,
                        uint32_t* counts) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_relabel<MODE, HUBS, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    set_attr_once(attr, k_relabel<MODE, HUBS, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_relabel<MODE, HUBS, STREAM><<<grid, kRlNT, smem, s>>>((const uint4*)I, (const uint4*)J, quads, label, hubs,
                                                     HubHash::make(n), n, (uint4*)I2, (uint4*)J2, counts);
 }

@@ -430,11 +430,8 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
         // x gathers of poorly ordered graphs depend on (c3 random labels: 0.417 ms
         // with the default, 0.367 ms pinned; BOBA order: 0.185 / 0.202 ms; the
         // scalar staging: 0.372 / 0.220 ms).
-        static bool carve = false;
-        if (!carve) {
-            cudaFuncSetAttribute(k_spmv_merge<T, sizeof(T) == 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 50);
-            carve = true;
-        }
+        static PerDeviceOnce carve;
+        set_attr_once(carve, k_spmv_merge<T, sizeof(T) == 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 50);
     }
     if (vec)
         k_spmv_merge<T, sizeof(T) == 4><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords,
