@@ -124,7 +124,7 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restr
     const uint32_t j0_32 = (uint32_t)j0;  // offsets are uint32: relative ends are exact mod 2^32
     for (uint32_t k = gt; k <= nrows; k += kSpNT)
         s_end[k] = (i0 + k < n) ? ld_stream_u32(offsets + i0 + 1 + k) - j0_32 : 0xFFFFFFFFu;
-    // VEC (fp32, unweighted, 16-byte aligned indices): the tile's indices are
+    // VEC (unweighted, 16-byte aligned indices): the tile's indices are
     // read as aligned quads from a0 = j0 & ~3 and the products stored as
     // quads at their a0-relative slot, so s_val[k + sh] holds item k
     const uint32_t sh = VEC ? (uint32_t)(j0 & 3) : 0u;
@@ -151,20 +151,26 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restr
             }
         }
         // every gather in flight before the first store (the random case is miss-bound)
-        const float* xf = reinterpret_cast<const float*>(x);
-        float4 v[QPT];
+        T v[QPT][4];
 #pragma unroll
         for (int u = 0; u < QPT; u++) {
             const uint32_t r = 4 * (gt + u * kSpNT);
-            v[u].x = r + 0 >= sh && r + 0 < span ? __ldg(xf + c[u].x) : 0.f;
-            v[u].y = r + 1 >= sh && r + 1 < span ? __ldg(xf + c[u].y) : 0.f;
-            v[u].z = r + 2 >= sh && r + 2 < span ? __ldg(xf + c[u].z) : 0.f;
-            v[u].w = r + 3 >= sh && r + 3 < span ? __ldg(xf + c[u].w) : 0.f;
+            v[u][0] = r + 0 >= sh && r + 0 < span ? __ldg(x + c[u].x) : T(0);
+            v[u][1] = r + 1 >= sh && r + 1 < span ? __ldg(x + c[u].y) : T(0);
+            v[u][2] = r + 2 >= sh && r + 2 < span ? __ldg(x + c[u].z) : T(0);
+            v[u][3] = r + 3 >= sh && r + 3 < span ? __ldg(x + c[u].w) : T(0);
         }
 #pragma unroll
         for (int u = 0; u < QPT; u++) {
             const uint32_t q = gt + u * kSpNT;
-            if (q < quads) reinterpret_cast<float4*>(s_val)[q] = v[u];
+            if (q < quads) {
+                if constexpr (sizeof(T) == 4) {
+                    reinterpret_cast<float4*>(s_val)[q] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                } else {
+                    reinterpret_cast<double2*>(s_val)[2 * q] = make_double2(v[u][0], v[u][1]);
+                    reinterpret_cast<double2*>(s_val)[2 * q + 1] = make_double2(v[u][2], v[u][3]);
+                }
+            }
         }
     } else {
         // all index loads, then all x gathers in flight together (nnz <= kSpTile)
@@ -423,18 +429,21 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
         k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
     // (A persistent variant with a 128 KB shared-memory copy of the hub prefix of x
     // was measured slower at c2/c3: the occupancy it costs outweighs the hits.)
-    const bool vec = sizeof(T) == 4 && !w && (reinterpret_cast<uintptr_t>(indices) & 15) == 0;
+    const bool vec = !w && (reinterpret_cast<uintptr_t>(indices) & 15) == 0;
     if (vec) {
-        // Pinned 50 % shared-memory carveout: left to the driver, the vector kernel's
-        // lower register count buys more resident CTAs at the cost of L1, which the
-        // x gathers of poorly ordered graphs depend on (c3 random labels: 0.417 ms
-        // with the default, 0.367 ms pinned; BOBA order: 0.185 / 0.202 ms; the
-        // scalar staging: 0.372 / 0.220 ms).
+        // Pinned shared-memory carveout: left to the driver, the vector kernel's
+        // register count buys more resident CTAs at the cost of L1, which the x
+        // gathers of poorly ordered graphs depend on.  c3 grid, (BOBA order,
+        // random order) per call:
+        //   fp32: driver default 0.185 / 0.417 ms, 50 % 0.202 / 0.367 (scalar staging 0.220 / 0.372)
+        //   fp64: 50 % 0.298 / 0.722, 66 % 0.271 / 0.775, 75 % 0.265 / 0.973,
+        //         100 % 0.277 / 1.79 (scalar staging, driver default: 0.248 / 1.80)
         static PerDeviceOnce carve;
-        set_attr_once(carve, k_spmv_merge<T, sizeof(T) == 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 50);
+        set_attr_once(carve, k_spmv_merge<T, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                      sizeof(T) == 4 ? 50 : 66);
     }
     if (vec)
-        k_spmv_merge<T, sizeof(T) == 4><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords,
+        k_spmv_merge<T, true><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords,
                                                                           tile_head, tile_tail, stop);
     else
         k_spmv_merge<T, false><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head,

@@ -286,9 +286,10 @@ def test_spmv_determinism_and_integer_exactness(dev):
     assert torch.equal(dev.spmv(off, idx, xr), dev.spmv(off, idx, xr))
 
 
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
 @pytest.mark.parametrize("n,mod", [(1, 1), (37, 2), (5000, 3), (70001, 1), (300000, 0)])
-def test_spmv_vector_staging_edges(dev, n, mod):
-    """fp32 SpMV: the 16-byte staging path (aligned indices) and the scalar
+def test_spmv_vector_staging_edges(dev, n, mod, dtype):
+    """SpMV (fp32 and fp64): the 16-byte staging path (aligned indices) and the scalar
     one (indices one element off alignment) give bitwise the same y, equal to
     the oracle on integer data; m = mod (mod 4) leaves a partial last quad;
     rows mix empty, short and tile-spanning hub rows."""
@@ -303,7 +304,7 @@ def test_spmv_vector_staging_edges(dev, n, mod):
     off = np.zeros(n + 1, np.int64)
     off[1:] = np.cumsum(deg)
     idx = rng.integers(0, n, m)
-    x = rng.integers(0, 4, n).astype(np.float32)
+    x = rng.integers(0, 4, n).astype(dtype)
     t_off = torch.from_numpy(off.astype(np.uint32).view(np.int32)).cuda()
     aligned = torch.from_numpy(idx.astype(np.uint32).view(np.int32)).cuda()
     buf = torch.empty(m + 1, dtype=torch.int32, device="cuda")
