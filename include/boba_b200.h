@@ -120,6 +120,18 @@ size_t boba_spmv_workspace_size(uint32_t n, uint64_t m);
 int boba_spmv(const uint32_t *offsets, const uint32_t *indices, const float *weights,
               const float *x, float *y, uint32_t n, uint64_t m, void *workspace,
               size_t workspace_bytes, void *stream);
+/* Same, for iterative callers (the k SpMV iterations of the reference bench,
+ * bench.py:152-156): reuse_partition != 0 skips the merge-path partition
+ * (one binary search per tile) and uses the one the previous call left in
+ * `workspace` -- the caller guarantees that call had the same offsets
+ * contents, n and m.  The partition depends on the structure only. */
+int boba_spmv_ex(const uint32_t *offsets, const uint32_t *indices, const float *weights, const float *x,
+                 float *y, uint32_t n, uint64_t m, void *workspace, size_t workspace_bytes,
+                 int reuse_partition, void *stream);
+int boba_spmv_f64_ex(const uint32_t *offsets, const uint32_t *indices, const double *weights, const double *x,
+                     double *y, uint32_t n, uint64_t m, void *workspace, size_t workspace_bytes,
+                     int reuse_partition, void *stream);
+
 /* Same in float64 -- the reference's own precision (kernels.py:30-52); the
  * drop-in spmv_pull uses it.  Same workspace size. */
 int boba_spmv_f64(const uint32_t *offsets, const uint32_t *indices, const double *weights,

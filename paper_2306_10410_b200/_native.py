@@ -51,6 +51,8 @@ SIGNATURES = {
     "boba_spmv_workspace_size": ([_U32, _U64], _SZ),
     "boba_spmv": ([_P, _P, _P, _P, _P, _U32, _U64, _P, _SZ, _P], _I),
     "boba_spmv_f64": ([_P, _P, _P, _P, _P, _U32, _U64, _P, _SZ, _P], _I),
+    "boba_spmv_ex": ([_P, _P, _P, _P, _P, _U32, _U64, _P, _SZ, _I, _P], _I),
+    "boba_spmv_f64_ex": ([_P, _P, _P, _P, _P, _U32, _U64, _P, _SZ, _I, _P], _I),
     "boba_reorder_to_csr_workspace_size": ([_U64, _U32, _I], _SZ),
     "boba_reorder_to_csr": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], _I),
     "boba_reorder_to_csr_timed": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P, _P], _I),

@@ -196,21 +196,33 @@ int boba_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uin
 
 size_t boba_spmv_workspace_size(uint32_t n, uint64_t m) { return boba::spmv_workspace_bytes(n, m); }
 
-int boba_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y, uint32_t n,
-              uint64_t m, void* ws, size_t ws_bytes, void* stream) {
+int boba_spmv_ex(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,
+                 uint32_t n, uint64_t m, void* ws, size_t ws_bytes, int reuse_partition, void* stream) {
     if (n == 0) return BOBA_OK;
     REQUIRE(offsets && x && y && ws && (indices || m == 0), "boba_spmv: NULL argument");
-    REQUIRE((uint64_t)n + m < 0xFFFFFFFFull * 2048ull, "boba_spmv: too large");
-    return cuda_status(boba::launch_spmv(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream)), "boba_spmv");
+    REQUIRE((uint64_t)n + m < 0xFFFFFFFFull * 1024ull, "boba_spmv: too large");
+    return cuda_status(boba::launch_spmv(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream), reuse_partition != 0),
+                       "boba_spmv");
+}
+
+int boba_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y, uint32_t n,
+              uint64_t m, void* ws, size_t ws_bytes, void* stream) {
+    return boba_spmv_ex(offsets, indices, w, x, y, n, m, ws, ws_bytes, 0, stream);
+}
+
+int boba_spmv_f64_ex(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x, double* y,
+                     uint32_t n, uint64_t m, void* ws, size_t ws_bytes, int reuse_partition, void* stream) {
+    if (n == 0) return BOBA_OK;
+    REQUIRE(offsets && x && y && ws && (indices || m == 0), "boba_spmv_f64: NULL argument");
+    REQUIRE((uint64_t)n + m < 0xFFFFFFFFull * 1024ull, "boba_spmv_f64: too large");
+    return cuda_status(
+        boba::launch_spmv_f64(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream), reuse_partition != 0),
+        "boba_spmv_f64");
 }
 
 int boba_spmv_f64(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x, double* y,
                   uint32_t n, uint64_t m, void* ws, size_t ws_bytes, void* stream) {
-    if (n == 0) return BOBA_OK;
-    REQUIRE(offsets && x && y && ws && (indices || m == 0), "boba_spmv_f64: NULL argument");
-    REQUIRE((uint64_t)n + m < 0xFFFFFFFFull * 2048ull, "boba_spmv_f64: too large");
-    return cuda_status(boba::launch_spmv_f64(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream)),
-                       "boba_spmv_f64");
+    return boba_spmv_f64_ex(offsets, indices, w, x, y, n, m, ws, ws_bytes, 0, stream);
 }
 
 size_t boba_reorder_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted) {

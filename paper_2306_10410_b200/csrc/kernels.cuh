@@ -40,9 +40,9 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
 
 size_t spmv_workspace_bytes(uint32_t n, uint64_t m);
 cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,
-                        uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s);
+                        uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s, bool partitioned = false);
 cudaError_t launch_spmv_f64(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x,
-                            double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s);
+                            double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s, bool partitioned = false);
 
 cudaError_t launch_rmat(int scale, uint64_t e0, uint64_t count, uint64_t seed, uint32_t* I, uint32_t* J,
                         int num_sms, cudaStream_t s);

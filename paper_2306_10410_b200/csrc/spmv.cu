@@ -458,13 +458,14 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
 }
 
 cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,
-                        uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s) {
-    return launch_spmv_t<float>(offsets, indices, w, x, y, n, m, ws, ws_bytes, s);
+                        uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s, bool partitioned) {
+    return launch_spmv_t<float>(offsets, indices, w, x, y, n, m, ws, ws_bytes, s, nullptr, partitioned);
 }
 
 cudaError_t launch_spmv_f64(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x,
-                            double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s) {
-    return launch_spmv_t<double>(offsets, indices, w, x, y, n, m, ws, ws_bytes, s);
+                            double* y, uint32_t n, uint64_t m, void* ws, size_t ws_bytes, cudaStream_t s,
+                            bool partitioned) {
+    return launch_spmv_t<double>(offsets, indices, w, x, y, n, m, ws, ws_bytes, s, nullptr, partitioned);
 }
 
 cudaError_t launch_spmv_f64_iter(const uint32_t* offsets, const uint32_t* indices, const double* w, const double* x,

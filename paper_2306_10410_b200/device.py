@@ -152,9 +152,11 @@ def coo_to_csr(I2: torch.Tensor, J2: torch.Tensor, n: int, weights: torch.Tensor
 
 def spmv(offsets: torch.Tensor, indices: torch.Tensor, x: torch.Tensor,
          weights: torch.Tensor | None = None, out: torch.Tensor | None = None,
-         ws: torch.Tensor | None = None) -> torch.Tensor:
+         ws: torch.Tensor | None = None, reuse_partition: bool = False) -> torch.Tensor:
     """Phase 5 (reference kernels.py:30-52).  Computes in x's precision:
-    float32 (the benchmarked path) or float64 (the reference's)."""
+    float32 (the benchmarked path) or float64 (the reference's).
+    reuse_partition: the previous call with this `ws` had the same CSR
+    structure; its merge-path partition is reused (iterative callers)."""
     n = offsets.numel() - 1
     m = indices.numel()
     f64 = x.dtype == torch.float64
@@ -163,10 +165,13 @@ def spmv(offsets: torch.Tensor, indices: torch.Tensor, x: torch.Tensor,
     if weights is not None:
         weights = weights.to(dt).contiguous()
     y = out if out is not None else torch.empty(max(n, 1), dtype=dt, device=offsets.device)[:n]
+    if reuse_partition and ws is None:
+        raise ValueError("reuse_partition needs the workspace of the previous call")
     if ws is None:
         ws = _ws(N.lib.boba_spmv_workspace_size(n, m), offsets.device)
-    fn = N.lib.boba_spmv_f64 if f64 else N.lib.boba_spmv
-    N.check(fn(_p(offsets), _p(indices), _p(weights), _p(x), _p(y), n, m, _p(ws), ws.numel(), _s()))
+    fn = N.lib.boba_spmv_f64_ex if f64 else N.lib.boba_spmv_ex
+    N.check(fn(_p(offsets), _p(indices), _p(weights), _p(x), _p(y), n, m, _p(ws), ws.numel(), int(reuse_partition),
+               _s()))
     return y
 
 

@@ -284,6 +284,14 @@ def test_spmv_determinism_and_integer_exactness(dev):
     assert np.array_equal(y1.cpu().numpy().astype(np.float64), want)   # integer sums < 2^24: exact
     xr = torch.rand(n, device=I.device)
     assert torch.equal(dev.spmv(off, idx, xr), dev.spmv(off, idx, xr))
+    # iterative form: later calls reuse the first call's partition (boba_spmv_ex)
+    for x_ in (xr, xr.double()):
+        ws = dev.spmv_workspace(n, I.numel(), I.device)
+        dev.spmv(off, idx, x_, ws=ws)
+        x2 = x_ * 3 + 1
+        assert torch.equal(dev.spmv(off, idx, x2, ws=ws, reuse_partition=True), dev.spmv(off, idx, x2))
+    with pytest.raises(ValueError):
+        dev.spmv(off, idx, xr, reuse_partition=True)
 
 
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
