@@ -33,8 +33,11 @@ constexpr int kHubHistRows = 8192;
 // STREAM (label[] beyond L2): the edge streams are loaded and stored
 // evict-first and the label gathers marked evict-last, so the 17 GB of
 // streaming traffic at s26 does not push the table's lines out of L2.
-__device__ __forceinline__ uint32_t ld_label(const uint32_t* p, bool stream, unsigned long long pol) {
-    if (!stream) return __ldcg(p);
+// Without the hub table (n > 2^23) the L1 is free to cache hot labels (c5:
+// 2.25 -> 2.19 ms); with it, the 192 KB table leaves ~36 KB of L1 and caching
+// there costs more than it hits (c2: 0.40 -> 0.43 ms), so the gathers skip L1.
+__device__ __forceinline__ uint32_t ld_label(const uint32_t* p, bool stream, unsigned long long pol, bool l1 = false) {
+    if (!stream) return l1 ? __ldg(p) : __ldcg(p);
     uint32_t v;
     asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
@@ -75,7 +78,7 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ 
     if (STREAM) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     auto lookup = [&](uint32_t v) -> uint32_t {
         const uint32_t h = probe(v);
-        return h != 0xFFFFFFFFu ? h : ld_label(label + v, STREAM, pol);
+        return h != 0xFFFFFFFFu ? h : ld_label(label + v, STREAM, pol, !HUBS);
     };
     auto count = [&](uint32_t r) {
         if (r < (uint32_t)kHubHistRows)
