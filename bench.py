@@ -157,6 +157,50 @@ def host_graph(cfg):
     return n, lab[I], lab[J]
 
 
+def device_input(cfg, dev):
+    """The bench's input graph for `cfg` on `dev`: the device generator (twin
+    of oracle.rmat_edges / generate_grid), then randomize_labels with
+    LABEL_SEED (reference io.py:294-301).  Returns (n, m, I, J) as int32
+    tensors holding uint32 ids.  Also used by the parity tests, so the graph
+    checked there is exactly the graph timed here."""
+    import torch
+
+    import oracle
+    from paper_2306_10410_b200 import device as D
+
+    kind, p, _ = CONFIGS[cfg]
+    n, m = graph_size(cfg)
+    if kind == "rmat":
+        I0, J0 = D.generate_rmat(p["scale"], p["ef"], GEN_SEED, dev)
+    else:
+        I0, J0 = D.generate_grid(p["rows"], p["cols"], dev)
+    lab = torch.from_numpy(oracle.random_labels(n, LABEL_SEED).astype(np.int32)).to(dev)
+    I, J = D.gather(lab, I0), D.gather(lab, J0)
+    del I0, J0, lab
+    return n, m, I, J
+
+
+def host_input_u32(cfg, chunk=1 << 26):
+    """The same graph built on the host by the oracle's generators (uint32,
+    generated in chunks so s26 needs 8.6 GB, not 34 GB of int64)."""
+    import oracle
+
+    kind, p, _ = CONFIGS[cfg]
+    n, m = graph_size(cfg)
+    lab = oracle.random_labels(n, LABEL_SEED).astype(np.uint32)
+    I = np.empty(m, np.uint32)
+    J = np.empty(m, np.uint32)
+    if kind == "rmat":
+        for e0 in range(0, m, chunk):
+            e1 = min(m, e0 + chunk)
+            a, b = oracle.rmat_edges(p["scale"], p["ef"], GEN_SEED, e0, e1)
+            I[e0:e1], J[e0:e1] = lab[a], lab[b]
+    else:
+        a, b = oracle.grid_edges(p["rows"], p["cols"])
+        I[:], J[:] = lab[a], lab[b]
+    return n, I, J
+
+
 def cpu_pipeline_time(n, I, J, threads):
     import oracle
 

@@ -63,6 +63,7 @@ def _load():
         "oracle_spmv_pull": ([_P, _P, _P, _P, _I64, _P], None),
         "oracle_rmat_edges": ([ctypes.c_int, _I64, ctypes.c_uint64, _I64, _I64, _P, _P], None),
         "oracle_grid_edges": ([_I64, _I64, _P, _P], None),
+        "oracle_verify_pipeline_u32": ([_P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -256,6 +257,31 @@ def pipeline(I, J, n, threads=0, weights=None):
     I2, J2 = apply_permutation(I, J, label)
     offsets, indices, w2 = coo_to_csr(I2, J2, n, weights)
     return order, label, I2, J2, offsets, indices, w2
+
+
+VERIFY_ARRAYS = ("order", "label", "I2", "J2", "offsets", "indices")
+
+
+def verify_pipeline_u32(I, J, n, order=None, label=None, I2=None, J2=None, offsets=None, indices=None):
+    """Streaming uint32 check of a device pipeline result against the
+    reference semantics (first_hit_order_sequential -> label ->
+    apply_permutation -> coo_to_csr; see oracle_verify_pipeline_u32) at
+    sizes where the int64 functions above would not fit in host memory.
+    Returns {array name: first differing index} for every array that differs
+    (empty dict = bit-exact)."""
+    def u32(a):
+        return None if a is None else np.ascontiguousarray(a).view(np.uint32)
+
+    I, J = u32(I), u32(J)
+    got = [u32(a) for a in (order, label, I2, J2, offsets, indices)]
+    for a, size in zip(got, (n, n, I.size, I.size, n + 1, I.size)):
+        if a is not None and a.size != size:
+            raise ValueError("result array has the wrong size")
+    first = np.empty(6, np.int64)
+    bad = _load().oracle_verify_pipeline_u32(_ptr(I), _ptr(J), I.size, int(n), *[_ptr(a) for a in got], _ptr(first))
+    if bad < 0:
+        raise MemoryError("oracle_verify_pipeline_u32: allocation failed")
+    return {VERIFY_ARRAYS[k]: int(first[k]) for k in range(6) if bad & (1 << k)}
 
 
 def nbr(offsets, indices, line_size=32):

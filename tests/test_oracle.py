@@ -146,3 +146,24 @@ def test_against_live_reference():
         I2, J2 = oracle.apply_permutation(I, J, oracle.label_from_order(order))
         off, idx, _ = oracle.coo_to_csr(I2, J2, n)
         assert np.array_equal(off, csr.offsets) and np.array_equal(idx, csr.indices)
+
+
+def test_streaming_u32_verifier_against_golden(kat, fuzz, medium):
+    """oracle.verify_pipeline_u32 (the BASELINE-size checker) accepts the
+    reference's own outputs and pinpoints a corrupted entry in each array."""
+    u = lambda a: np.asarray(a, dtype=np.int64).astype(np.uint32)  # noqa: E731
+    cases = list(kat) + [fuzz.case(i) for i in range(0, fuzz.count, 5)] + list(medium)
+    for c in cases:
+        n = c["n"]
+        got = dict(order=u(c["order"]), label=u(c["label"]), I2=u(c["I2"]), J2=u(c["J2"]),
+                   offsets=u(c["offsets"]), indices=u(c["indices"]))
+        assert oracle.verify_pipeline_u32(u(c["I"]), u(c["J"]), n, **got) == {}
+        for name, arr in got.items():
+            if arr.size < 2 or (name == "offsets" and c["I"].size == 0):
+                continue
+            bad = dict(got)
+            bad[name] = arr.copy()
+            k = arr.size // 2
+            bad[name][k] ^= 1
+            res = oracle.verify_pipeline_u32(u(c["I"]), u(c["J"]), n, **bad)
+            assert name in res, (name, res)
