@@ -65,8 +65,11 @@ int boba_first_occurrence(const uint32_t *I, const uint32_t *J, uint64_t m, uint
  * gives exactly boba_first_occurrence of the whole list -- the reference's
  * chunk-local-min merge, _parallel.py:139-162.
  * workspace (may be NULL; boba_first_occurrence_workspace_size() bytes)
- * enables the two-stage sweep with the shared-memory SeenSet of hubs. */
+ * enables the two-stage sweep with the shared-memory SeenSet of hubs; with
+ * boba_first_occurrence_shard_workspace_size(n) bytes, also the wave-guarded
+ * sweep the fused single-GPU call uses beyond L2 (n > 2^24). */
 size_t boba_first_occurrence_workspace_size(void);
+size_t boba_first_occurrence_shard_workspace_size(uint32_t n);
 int boba_first_occurrence_shard(const uint32_t *I, const uint32_t *J, uint64_t m_local,
                                 uint64_t m_global, uint64_t e0, uint32_t n, uint32_t *first,
                                 int relaxed, void *workspace, size_t workspace_bytes, void *stream);
@@ -168,6 +171,9 @@ int boba_reorder_to_csr_graph_create(const uint32_t *I, const uint32_t *J, uint6
                                      size_t workspace_bytes, boba_graph **out);
 int boba_graph_launch(boba_graph *graph, void *stream);
 void boba_reorder_to_csr_graph_destroy(boba_graph *graph);
+/* Number of kernel launches one boba_graph_launch replays (the graph's
+ * kernel nodes; memset nodes are not counted). */
+int boba_graph_kernel_nodes(const boba_graph *graph, uint64_t *count);
 
 /* --- Host-buffer pipeline (end to end) ----------------------------------
  * A context owns device buffers for graphs up to (max_m, max_n) on the
@@ -209,6 +215,14 @@ int boba_nbr(const uint32_t *offsets, const uint32_t *indices, uint32_t n, uint6
 int boba_narrow_ids(const int64_t *in, uint64_t count, uint64_t bound, uint32_t *out,
                     int64_t *bad_index, void *stream);
 int boba_widen_ids(const uint32_t *in, uint64_t count, int64_t *out, void *stream);
+/* Host int64 ids -> device uint32 (narrowed on host threads into pinned
+ * staging, chunked so narrowing overlaps the copies), with the same range
+ * check as boba_narrow_ids; and device uint32 -> host int64 (widened on host
+ * threads while the next chunk copies).  Both return once `host` may be
+ * reused / read (synchronous on `stream`).  The drop-in's transfers. */
+int boba_host_to_device_ids(const int64_t *host, uint64_t count, uint64_t bound, uint32_t *dev,
+                            int64_t *bad_index, void *stream);
+int boba_device_to_host_ids(const uint32_t *dev, uint64_t count, int64_t *host, void *stream);
 /* offsets[0..n] = exclusive prefix sum of counts[0..n) (offsets[n] = total):
  * np.cumsum of graph.py:270-272 on the device. */
 size_t boba_exclusive_scan_workspace_size(uint64_t count);
@@ -234,25 +248,68 @@ int boba_compact_relabel(const uint32_t *first, uint64_t m_global, uint32_t n, c
                          const uint32_t *J, uint64_t m, uint32_t *order, uint32_t *label, uint32_t *I2,
                          uint32_t *J2, void *workspace, size_t workspace_bytes, void *stream);
 
-/* Row-partitioned CSR across ranks (sharded.py; replaces the reference's
- * single-process coo_to_csr, graph.py:253-277, for a row range).
- * boba_adjacent_diff_u32: out[i] = in[i+1] - in[i] for i < count (per-row
- * counts from CSR offsets).  boba_merge_rows: `recv` holds `parts` senders'
- * runs back to back in rank order, each run = that sender's entries for rows
- * [0, rows) in row order with counts[k * rows + r] entries for row r; writes
- * row r of the output at out_offsets[r] as sender 0's entries, then sender
- * 1's, ... (global edge order when senders hold contiguous edge shards).
- * recv_len = the sum of the counts. */
-int boba_adjacent_diff_u32(const uint32_t *in, uint64_t count, uint32_t *out, void *stream);
-size_t boba_merge_rows_workspace_size(int parts, uint32_t rows, uint64_t recv_len);
-int boba_merge_rows(const uint32_t *recv, uint64_t recv_len, int parts, uint32_t rows,
-                    const uint32_t *counts, const uint32_t *out_offsets, uint32_t *out, void *workspace,
-                    size_t workspace_bytes, void *stream);
 size_t boba_range_partition_workspace_size(uint64_t m, int parts);
 int boba_range_partition(const uint32_t *keys, const uint32_t *vals, uint64_t m,
                          const uint32_t *bounds, int parts, uint32_t *keys_out, uint32_t *vals_out,
                          uint32_t *counts_out, void *workspace, size_t workspace_bytes,
                          void *stream);
+/* As boba_range_partition; relative_keys != 0 writes each key minus its
+ * part's first row (bounds[p]), i.e. row ids local to the owner; counts_out
+ * may be NULL. */
+int boba_range_partition_ex(const uint32_t *keys, const uint32_t *vals, uint64_t m,
+                            const uint32_t *bounds, int parts, int relative_keys, uint32_t *keys_out,
+                            uint32_t *vals_out, uint32_t *counts_out, void *workspace,
+                            size_t workspace_bytes, void *stream);
+
+/* --- Multi-GPU phases (sharded.py; one process per GPU) -------------------
+ * The collectives between these calls belong to the caller: NCCL through
+ * torch.distributed in sharded.py; a C/C++ caller issues the same
+ * ncclAllReduce / ncclAllGather / ncclSend+ncclRecv on its own ncclComm_t
+ * (the sequence is spelled out in INTEGRATION.md §4).  Rank r of P holds the
+ * contiguous edges [e0, e0 + m_local) of the m_global-edge list, i.e.
+ * positions [e0, e0 + m_local) of I and [m_global + e0, ...) of J.
+ *
+ * Phase 1: boba_first_occurrence_shard, boba_bias_u32,
+ *   [allreduce-MIN over n int32], boba_bias_u32.
+ * Phase 2 (compact_ranks, _parallel.py:178-201, split by position window):
+ *   boba_compact_shard_mark: marks the vertices whose first position lies in
+ *     this rank's windows; counts[2] (device) = how many were first seen in
+ *     its I window and in its J window.
+ *   [allgather of counts -> all_counts[2P], rank-major]
+ *   boba_compact_shard_assign (same workspace, untouched since _mark):
+ *     label_partial[v] = global rank of each owned vertex, 0 for the other
+ *     seen vertices; never-seen vertices get n_seen + their ascending rank on
+ *     rank 0 and 0 elsewhere.
+ *   [allreduce-SUM of label_partial over n words -> label, replicated]
+ *   boba_order_from_label: order[label[v]] = v, plus (hubs != NULL,
+ *     boba_hub_table_bytes()) the hub label table of the smallest labels.
+ * Phase 3 (apply_permutation, graph.py:280-289): boba_relabel_hubs.
+ * Phase 4 (coo_to_csr, graph.py:253-277, rows split by range):
+ *   boba_row_cut_hist: coarse histogram of the local rows
+ *     (boba_row_cut_buckets(n) words, bucket = row >> max(0, bits(n-1) - 15)).
+ *   [allreduce-SUM of the histogram]
+ *   boba_row_cut(global hist, local hist): out[3P+2] = row bounds b[0..P]
+ *     (edge-balanced, on bucket boundaries), offsets[b_k] (P+1 words) and the
+ *     edges this rank sends to each owner (P words).
+ *   boba_range_partition_ex(bounds = out, relative_keys = 1): send buffers.
+ *   [all-to-all of keys and of values, in rank order]
+ *   boba_coo_to_csr on the received pairs (rows local to [b_r, b_r+1)). */
+size_t boba_compact_shard_workspace_size(uint64_t m_local, uint32_t n);
+int boba_compact_shard_mark(const uint32_t *first, uint32_t n, uint64_t m_global, uint64_t e0,
+                            uint64_t m_local, uint32_t *counts, void *workspace, size_t workspace_bytes,
+                            void *stream);
+int boba_compact_shard_assign(const uint32_t *first, uint32_t n, uint64_t m_global, uint64_t e0,
+                              uint64_t m_local, const uint32_t *all_counts, int world, int rank,
+                              uint32_t *label_partial, void *workspace, size_t workspace_bytes, void *stream);
+size_t boba_hub_table_bytes(void);
+int boba_order_from_label(const uint32_t *label, uint32_t n, uint32_t *order, void *hubs, void *stream);
+int boba_relabel_hubs(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n, const uint32_t *label,
+                      const void *hubs, uint32_t *I2, uint32_t *J2, void *stream);
+uint32_t boba_row_cut_buckets(uint32_t n);
+int boba_row_cut_hist(const uint32_t *rows, uint64_t m_local, uint32_t n, uint32_t *hist, void *stream);
+int boba_row_cut(const uint32_t *hist_global, const uint32_t *hist_local, uint32_t n, uint64_t m_global,
+                 int world, uint32_t *out, void *stream);
+
 /* out[i] = src[idx[i]] (permutation application on vertex arrays). */
 int boba_gather_u32(const uint32_t *src, const uint32_t *idx, uint64_t count, uint32_t *out,
                     void *stream);

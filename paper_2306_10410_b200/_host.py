@@ -1,19 +1,29 @@
 """numpy <-> device glue for the reference-shaped API.
 
 The reference works on host int64 arrays; the kernels on device uint32.
-Each helper copies its inputs to the current CUDA device once, narrows them
-there (with the reference's [0, n) range check), runs the C-ABI phase and
-widens the results back to int64 on the device before a single D2H copy.
+Ids cross PCIe as uint32: boba_host_to_device_ids narrows on host threads
+into pinned staging (with the reference's [0, n) range check) while earlier
+chunks copy, boba_device_to_host_ids widens on host threads while later
+chunks copy.
+
+Arrays this package itself returned inside an immutable container (the
+relabelled COO of apply_permutation, the label of a Permutation from
+boba_parallel) keep a reference to their device copy, so the next call of
+the reference pipeline (apply_permutation -> coo_to_csr) does not upload
+them again.  Arrays a caller passed in are always uploaded.
 """
 
 from __future__ import annotations
 
-import warnings
+import ctypes
+import weakref
 
 import numpy as np
 import torch
 
+from . import _native as N
 from . import device as D
+from .errors import MalformedGraphError
 
 RANK_UNSET = np.iinfo(np.int64).max  # reference _parallel.py:31
 
@@ -22,18 +32,45 @@ def _dev():
     return D.require_cuda()
 
 
+_DEVICE_COPIES: dict = {}
+
+
+def remember(host_arr, dev: torch.Tensor) -> None:
+    """Record that `dev` (uint32 ids on the device) equals the read-only
+    host array `host_arr` this package created; forgotten with the array."""
+    key = id(host_arr)
+    _DEVICE_COPIES[key] = (weakref.ref(host_arr, lambda _r, k=key: _DEVICE_COPIES.pop(k, None)), dev)
+
+
+def _recall(host_arr):
+    e = _DEVICE_COPIES.get(id(host_arr))
+    if e is None or e[0]() is not host_arr:
+        return None
+    t = e[1]
+    return t if t.device == _dev() else None
+
+
 def to_device_ids(a, bound: int, name: str = "ids") -> torch.Tensor:
+    cached = _recall(a)
+    if cached is not None:
+        return cached
     arr = np.ascontiguousarray(a, dtype=np.int64)
-    with warnings.catch_warnings():   # frozen (read-only) container arrays: only read, copied to the device
-        warnings.simplefilter("ignore", UserWarning)
-        t = torch.from_numpy(arr).to(_dev())
-    return D.narrow_ids(t, bound, name)
+    out = torch.empty(arr.size, dtype=D.ID, device=_dev())
+    bad = ctypes.c_int64(-1)
+    rc = N.lib.boba_host_to_device_ids(ctypes.c_void_p(arr.ctypes.data), arr.size, int(bound), D._p(out),
+                                       ctypes.byref(bad), D._s())
+    if rc == N.BOBA_ERANGE:
+        i = int(bad.value)
+        raise MalformedGraphError(f"{name}[{i}] = {int(arr[i])} out of range for n = {bound}")
+    N.check(rc)
+    return out
 
 
 def to_host_ids(t: torch.Tensor) -> np.ndarray:
-    if t.numel() == 0:
-        return np.empty(0, dtype=np.int64)
-    return D.as_u32_to_i64(t).cpu().numpy()
+    out = np.empty(t.numel(), dtype=np.int64)
+    if t.numel():
+        N.check(N.lib.boba_device_to_host_ids(D._p(t), t.numel(), ctypes.c_void_p(out.ctypes.data), D._s()))
+    return out
 
 
 def first_to_ranks(first: torch.Tensor) -> np.ndarray:
@@ -51,13 +88,13 @@ def ranks_to_first(r) -> torch.Tensor:
 
 
 def boba(I, J, n: int, relaxed: bool = False):
-    """-> (r int64 with RANK_UNSET, order int64, label int64)."""
+    """-> (r int64 with RANK_UNSET, order int64, label int64, device label)."""
     if n == 0:
         e = np.empty(0, dtype=np.int64)
-        return e, e.copy(), e.copy()
+        return e, e.copy(), e.copy(), None
     dI, dJ = to_device_ids(I, n, "I"), to_device_ids(J, n, "J")
     first, order, label = D.boba_order(dI, dJ, n, relaxed)
-    return first_to_ranks(first), to_host_ids(order), to_host_ids(label)
+    return first_to_ranks(first), to_host_ids(order), to_host_ids(label), label
 
 
 def compact(r, I, J, n: int):
@@ -70,13 +107,14 @@ def compact(r, I, J, n: int):
 
 
 def relabel(I, J, label, n: int):
+    """-> (I2, J2 host int64, I2, J2 on the device)."""
     m = int(np.asarray(I).size)
     if m == 0:
-        return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.int64)
+        return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.int64), None, None
     dI, dJ = to_device_ids(I, n, "I"), to_device_ids(J, n, "J")
     dl = to_device_ids(label, max(n, 1), "label")
     I2, J2 = D.relabel(dI, dJ, dl, n)
-    return to_host_ids(I2), to_host_ids(J2)
+    return to_host_ids(I2), to_host_ids(J2), I2, J2
 
 
 def degrees(I, n: int) -> np.ndarray:

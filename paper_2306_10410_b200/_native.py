@@ -39,6 +39,7 @@ SIGNATURES = {
     "boba_last_error": ([], ctypes.c_char_p),
     "boba_first_occurrence": ([_P, _P, _U64, _U32, _P, _I, _P], _I),
     "boba_first_occurrence_workspace_size": ([], _SZ),
+    "boba_first_occurrence_shard_workspace_size": ([_U32], _SZ),
     "boba_first_occurrence_shard": ([_P, _P, _U64, _U64, _U64, _U32, _P, _I, _P, _SZ, _P], _I),
     "boba_compact_workspace_size": ([_U64, _U32], _SZ),
     "boba_compact": ([_P, _U64, _U32, _P, _P, _P, _P, _SZ, _P], _I),
@@ -61,18 +62,28 @@ SIGNATURES = {
     "boba_ctx_reorder_to_csr_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P], _I),
     "boba_ctx_submit_host": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_U64)], _I),
     "boba_ctx_wait": ([_P, _U64], _I),
-    "boba_adjacent_diff_u32": ([_P, _U64, _P, _P], _I),
     "boba_nbr_workspace_size": ([_U64, _U32], _SZ),
     "boba_nbr": ([_P, _P, _U32, _U64, _U32, _P, _P, _SZ, _P], _I),
     "boba_compact_relabel_workspace_size": ([_U64, _U32], _SZ),
     "boba_compact_relabel": ([_P, _U64, _U32, _P, _P, _U64, _P, _P, _P, _P, _P, _SZ, _P], _I),
-    "boba_merge_rows_workspace_size": ([_I, _U32, _U64], _SZ),
-    "boba_merge_rows": ([_P, _U64, _I, _U32, _P, _P, _P, _P, _SZ, _P], _I),
+    "boba_range_partition_ex": ([_P, _P, _U64, _P, _I, _I, _P, _P, _P, _P, _SZ, _P], _I),
+    "boba_compact_shard_workspace_size": ([_U64, _U32], _SZ),
+    "boba_compact_shard_mark": ([_P, _U32, _U64, _U64, _U64, _P, _P, _SZ, _P], _I),
+    "boba_compact_shard_assign": ([_P, _U32, _U64, _U64, _U64, _P, _I, _I, _P, _P, _SZ, _P], _I),
+    "boba_hub_table_bytes": ([], _SZ),
+    "boba_order_from_label": ([_P, _U32, _P, _P, _P], _I),
+    "boba_relabel_hubs": ([_P, _P, _U64, _U32, _P, _P, _P, _P, _P], _I),
+    "boba_row_cut_buckets": ([_U32], _U32),
+    "boba_row_cut_hist": ([_P, _U64, _U32, _P, _P], _I),
+    "boba_row_cut": ([_P, _P, _U32, _U64, _I, _P, _P], _I),
     "boba_reorder_to_csr_graph_create": ([_P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ,
                                           ctypes.POINTER(_P)], _I),
     "boba_graph_launch": ([_P, _P], _I),
     "boba_reorder_to_csr_graph_destroy": ([_P], None),
+    "boba_graph_kernel_nodes": ([_P, _P], _I),
     "boba_narrow_ids": ([_P, _U64, _U64, _P, ctypes.POINTER(ctypes.c_int64), _P], _I),
+    "boba_host_to_device_ids": ([_P, _U64, _U64, _P, ctypes.POINTER(ctypes.c_int64), _P], _I),
+    "boba_device_to_host_ids": ([_P, _U64, _P, _P], _I),
     "boba_widen_ids": ([_P, _U64, _P, _P], _I),
     "boba_exclusive_scan_workspace_size": ([_U64], _SZ),
     "boba_exclusive_scan_u32": ([_P, _U32, _P, _P, _SZ, _P], _I),

@@ -32,7 +32,7 @@ def first_hit_sequential(I, J, n):
 
 def first_hit_order_sequential(I, J, n):
     """reference _parallel.py:111-136 -> (ranks, order)."""
-    r, order, _ = _host.boba(I, J, int(n))
+    r, order, _, _ = _host.boba(I, J, int(n))
     return r, order
 
 

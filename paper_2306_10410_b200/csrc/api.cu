@@ -3,7 +3,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <string>
+#include <unordered_map>
+#include <vector>
 
 #include "../../include/boba_b200.h"
 #include "common.cuh"
@@ -57,6 +60,44 @@ int check_sizes(uint64_t m, uint32_t n, const char* what) {
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
+// Makes `device` current for the scope and restores the caller's device.
+struct DeviceGuard {
+    int saved = -1;
+    explicit DeviceGuard(int device) {
+        if (cudaGetDevice(&saved) != cudaSuccess) saved = -1;
+        if (saved != device) cudaSetDevice(device);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (saved >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != saved) cudaSetDevice(saved);
+    }
+};
+
+// SpMV partitions kept in a caller's workspace: which CSR each workspace was
+// last partitioned for, so reuse_partition = 1 with a workspace that holds
+// another matrix's partition (or none) is an error instead of a wrong walk.
+struct SpmvKey {
+    const void* offsets;
+    const void* indices;
+    uint32_t n;
+    uint64_t m;
+    bool operator==(const SpmvKey& o) const {
+        return offsets == o.offsets && indices == o.indices && n == o.n && m == o.m;
+    }
+};
+std::mutex g_spmv_mu;
+std::unordered_map<const void*, SpmvKey> g_spmv_parts;
+
+bool spmv_partition_ok(const void* ws, const SpmvKey& k, bool reuse) {
+    std::lock_guard<std::mutex> lock(g_spmv_mu);
+    if (!reuse) {
+        g_spmv_parts[ws] = k;
+        return true;
+    }
+    auto it = g_spmv_parts.find(ws);
+    return it != g_spmv_parts.end() && it->second == k;
+}
+
 }  // namespace
 
 // Captured pipelines: one fused reorder->CSR call on fixed buffers recorded
@@ -108,6 +149,10 @@ int boba_first_occurrence(const uint32_t* I, const uint32_t* J, uint64_t m, uint
 
 size_t boba_first_occurrence_workspace_size(void) { return boba::first_hit_workspace_bytes(); }
 
+size_t boba_first_occurrence_shard_workspace_size(uint32_t n) {
+    return align256(boba::first_hit_workspace_bytes()) + boba::first_hit_bits_workspace_bytes(n);
+}
+
 int boba_first_occurrence_shard(const uint32_t* I, const uint32_t* J, uint64_t m_local, uint64_t m_global,
                                 uint64_t e0, uint32_t n, uint32_t* first, int relaxed, void* ws, size_t ws_bytes,
                                 void* stream) {
@@ -117,8 +162,11 @@ int boba_first_occurrence_shard(const uint32_t* I, const uint32_t* J, uint64_t m
     REQUIRE(first || n == 0, "boba_first_occurrence_shard: first is NULL");
     REQUIRE((I && J) || m_local == 0, "boba_first_occurrence_shard: I/J is NULL");
     if (n == 0) return BOBA_OK;
+    void* bits_ws = nullptr;
+    if (ws && ws_bytes >= boba_first_occurrence_shard_workspace_size(n))
+        bits_ws = static_cast<char*>(ws) + align256(boba::first_hit_workspace_bytes());
     return cuda_status(boba::launch_first_hit_shard(I, J, m_local, m_global, e0, n, first, relaxed != 0, ws,
-                                                    num_sms(), S(stream)),
+                                                    num_sms(), S(stream), bits_ws),
                        "boba_first_occurrence_shard");
 }
 
@@ -201,6 +249,8 @@ int boba_spmv_ex(const uint32_t* offsets, const uint32_t* indices, const float* 
     if (n == 0) return BOBA_OK;
     REQUIRE(offsets && x && y && ws && (indices || m == 0), "boba_spmv: NULL argument");
     REQUIRE((uint64_t)n + m < 0xFFFFFFFFull * 1024ull, "boba_spmv: too large");
+    REQUIRE(spmv_partition_ok(ws, SpmvKey{offsets, indices, n, m}, reuse_partition != 0),
+            "boba_spmv: reuse_partition = 1 but this workspace was not partitioned for this CSR");
     return cuda_status(boba::launch_spmv(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream), reuse_partition != 0),
                        "boba_spmv");
 }
@@ -215,6 +265,8 @@ int boba_spmv_f64_ex(const uint32_t* offsets, const uint32_t* indices, const dou
     if (n == 0) return BOBA_OK;
     REQUIRE(offsets && x && y && ws && (indices || m == 0), "boba_spmv_f64: NULL argument");
     REQUIRE((uint64_t)n + m < 0xFFFFFFFFull * 1024ull, "boba_spmv_f64: too large");
+    REQUIRE(spmv_partition_ok(ws, SpmvKey{offsets, indices, n, m}, reuse_partition != 0),
+            "boba_spmv_f64: reuse_partition = 1 but this workspace was not partitioned for this CSR");
     return cuda_status(
         boba::launch_spmv_f64(offsets, indices, w, x, y, n, m, ws, ws_bytes, S(stream), reuse_partition != 0),
         "boba_spmv_f64");
@@ -317,6 +369,24 @@ int boba_graph_launch(boba_graph* g, void* stream) {
     return cuda_status(cudaGraphLaunch(g->exec, S(stream)), "boba_graph_launch");
 }
 
+int boba_graph_kernel_nodes(const boba_graph* g, uint64_t* count) {
+    REQUIRE(g && g->graph && count, "boba_graph_kernel_nodes: NULL argument");
+    size_t num = 0;
+    cudaError_t e = cudaGraphGetNodes(g->graph, nullptr, &num);
+    if (e != cudaSuccess) return cuda_status(e, "boba_graph_kernel_nodes");
+    std::vector<cudaGraphNode_t> nodes(num);
+    if (num) e = cudaGraphGetNodes(g->graph, nodes.data(), &num);
+    uint64_t k = 0;
+    for (size_t i = 0; e == cudaSuccess && i < num; i++) {
+        cudaGraphNodeType t;
+        e = cudaGraphNodeGetType(nodes[i], &t);
+        k += e == cudaSuccess && t == cudaGraphNodeTypeKernel;
+    }
+    if (e != cudaSuccess) return cuda_status(e, "boba_graph_kernel_nodes");
+    *count = k;
+    return BOBA_OK;
+}
+
 void boba_reorder_to_csr_graph_destroy(boba_graph* g) {
     if (!g) return;
     if (g->exec) cudaGraphExecDestroy(g->exec);
@@ -360,6 +430,7 @@ int boba_ctx_create(uint64_t max_m, uint32_t max_n, boba_ctx** out) {
 
 void boba_ctx_destroy(boba_ctx* c) {
     if (!c) return;
+    DeviceGuard guard(c->device);
     for (cudaStream_t st : {c->stream, c->h2d, c->d2h})
         if (st) cudaStreamSynchronize(st);
     for (boba_slot& S : c->slot) {
@@ -379,6 +450,7 @@ int boba_ctx_submit_host(boba_ctx* c, const uint32_t* I_h, const uint32_t* J_h, 
                          uint32_t* order_h, uint32_t* label_h, uint32_t* I2_h, uint32_t* J2_h, uint32_t* offsets_h,
                          uint32_t* indices_h, uint64_t* ticket) {
     REQUIRE(c, "boba_ctx_submit_host: NULL context");
+    DeviceGuard guard(c->device);
     REQUIRE(m <= c->max_m && n <= c->max_n, "boba_ctx_submit_host: graph exceeds the context capacity");
     REQUIRE(order_h && label_h && offsets_h && (indices_h || m == 0) && ((I_h && J_h) || m == 0),
             "boba_ctx_submit_host: NULL host buffer");
@@ -422,6 +494,7 @@ int boba_ctx_submit_host(boba_ctx* c, const uint32_t* I_h, const uint32_t* J_h, 
 
 int boba_ctx_wait(boba_ctx* c, uint64_t ticket) {
     REQUIRE(c, "boba_ctx_wait: NULL context");
+    DeviceGuard guard(c->device);
     REQUIRE(ticket < c->submitted, "boba_ctx_wait: ticket %llu was never submitted", (unsigned long long)ticket);
     // the slot's d2h_done event is the newest graph in that slot; graphs of a
     // slot complete in submission order, so waiting on it covers `ticket`
@@ -459,6 +532,26 @@ int boba_narrow_ids(const int64_t* in, uint64_t count, uint64_t bound, uint32_t*
     return BOBA_OK;
 }
 
+int boba_host_to_device_ids(const int64_t* host, uint64_t count, uint64_t bound, uint32_t* dev, int64_t* bad_index,
+                            void* stream) {
+    REQUIRE((host && dev) || count == 0, "boba_host_to_device_ids: NULL argument");
+    REQUIRE(bound <= 0x100000000ull, "boba_host_to_device_ids: bound exceeds uint32");
+    int64_t bad = -1;
+    if (int rc = cuda_status(boba::host_h2d_ids(host, count, bound, dev, &bad, S(stream)), "boba_host_to_device_ids"))
+        return rc;
+    if (bad >= 0) {
+        if (bad_index) *bad_index = bad;
+        return fail(BOBA_ERANGE, "boba_host_to_device_ids: element %lld out of range [0, %llu)", (long long)bad,
+                    (unsigned long long)bound);
+    }
+    return BOBA_OK;
+}
+
+int boba_device_to_host_ids(const uint32_t* dev, uint64_t count, int64_t* host, void* stream) {
+    REQUIRE((host && dev) || count == 0, "boba_device_to_host_ids: NULL argument");
+    return cuda_status(boba::host_d2h_ids(dev, count, host, S(stream)), "boba_device_to_host_ids");
+}
+
 int boba_widen_ids(const uint32_t* in, uint64_t count, int64_t* out, void* stream) {
     REQUIRE((in && out) || count == 0, "boba_widen_ids: NULL argument");
     return cuda_status(boba::launch_widen(in, count, out, num_sms(), S(stream)), "boba_widen_ids");
@@ -493,37 +586,87 @@ size_t boba_range_partition_workspace_size(uint64_t m, int parts) {
     return boba::range_partition_workspace_bytes(m, parts);
 }
 
-int boba_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds, int parts,
-                         uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out, void* ws, size_t ws_bytes,
-                         void* stream) {
+int boba_range_partition_ex(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds,
+                            int parts, int relative_keys, uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out,
+                            void* ws, size_t ws_bytes, void* stream) {
     REQUIRE(parts >= 1 && parts <= 256, "boba_range_partition: parts must be in [1, 256]");
-    REQUIRE(bounds && counts_out && ws, "boba_range_partition: NULL argument");
+    REQUIRE(bounds && ws, "boba_range_partition: NULL argument");
     REQUIRE((keys && vals && keys_out && vals_out) || m == 0, "boba_range_partition: NULL edge arrays");
     REQUIRE(m < 0xFFFFFFFFull, "boba_range_partition: m too large");
     return cuda_status(boba::launch_range_partition(keys, vals, m, bounds, parts, keys_out, vals_out, counts_out, ws,
-                                                    ws_bytes, num_sms(), S(stream)),
+                                                    ws_bytes, num_sms(), S(stream), relative_keys != 0),
                        "boba_range_partition");
 }
 
-int boba_adjacent_diff_u32(const uint32_t* in, uint64_t count, uint32_t* out, void* stream) {
-    REQUIRE((in && out) || count == 0, "boba_adjacent_diff_u32: NULL argument");
-    return cuda_status(boba::launch_adjacent_diff(in, count, out, num_sms(), S(stream)), "boba_adjacent_diff_u32");
+int boba_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds, int parts,
+                         uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out, void* ws, size_t ws_bytes,
+                         void* stream) {
+    REQUIRE(counts_out, "boba_range_partition: NULL counts_out");
+    return boba_range_partition_ex(keys, vals, m, bounds, parts, 0, keys_out, vals_out, counts_out, ws, ws_bytes,
+                                   stream);
 }
 
-size_t boba_merge_rows_workspace_size(int parts, uint32_t rows, uint64_t recv_len) {
-    return boba::merge_rows_workspace_bytes(parts, rows, recv_len);
+size_t boba_compact_shard_workspace_size(uint64_t m_local, uint32_t n) {
+    return boba::compact_window_workspace_bytes(m_local, n);
 }
 
-int boba_merge_rows(const uint32_t* recv, uint64_t recv_len, int parts, uint32_t rows, const uint32_t* counts,
-                    const uint32_t* out_offsets, uint32_t* out, void* ws, size_t ws_bytes, void* stream) {
-    REQUIRE(parts >= 1, "boba_merge_rows: parts must be positive");
-    REQUIRE((uint64_t)parts * rows < 0xFFFFFFFFull && recv_len < 0xFFFFFFFFull, "boba_merge_rows: too large");
-    REQUIRE(ws && (rows == 0 || (counts && out_offsets)), "boba_merge_rows: NULL argument");
-    REQUIRE((recv && out) || recv_len == 0, "boba_merge_rows: NULL entries");
-    REQUIRE(ws_bytes >= boba::merge_rows_workspace_bytes(parts, rows, recv_len), "boba_merge_rows: workspace too small");
-    return cuda_status(boba::launch_merge_rows(recv, recv_len, parts, rows, counts, out_offsets, out, ws, ws_bytes,
-                                               num_sms(), S(stream)),
-                       "boba_merge_rows");
+int boba_compact_shard_mark(const uint32_t* first, uint32_t n, uint64_t m_global, uint64_t e0, uint64_t m_local,
+                            uint32_t* counts, void* ws, size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m_global, n, "boba_compact_shard_mark")) return rc;
+    REQUIRE(e0 + m_local <= m_global, "boba_compact_shard_mark: shard outside [0, m_global)");
+    REQUIRE(counts && ws && (first || n == 0), "boba_compact_shard_mark: NULL argument");
+    REQUIRE(ws_bytes >= boba::compact_window_workspace_bytes(m_local, n), "boba_compact_shard_mark: workspace too small");
+    return cuda_status(boba::launch_compact_window_mark(first, n, m_global, e0, m_local, counts, ws, ws_bytes,
+                                                        num_sms(), S(stream)),
+                       "boba_compact_shard_mark");
+}
+
+int boba_compact_shard_assign(const uint32_t* first, uint32_t n, uint64_t m_global, uint64_t e0, uint64_t m_local,
+                              const uint32_t* all_counts, int world, int rank, uint32_t* label_partial, void* ws,
+                              size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m_global, n, "boba_compact_shard_assign")) return rc;
+    REQUIRE(world >= 1 && rank >= 0 && rank < world, "boba_compact_shard_assign: bad rank/world");
+    REQUIRE(e0 + m_local <= m_global, "boba_compact_shard_assign: shard outside [0, m_global)");
+    REQUIRE(all_counts && ws && ((first && label_partial) || n == 0), "boba_compact_shard_assign: NULL argument");
+    REQUIRE(ws_bytes >= boba::compact_window_workspace_bytes(m_local, n),
+            "boba_compact_shard_assign: workspace too small");
+    return cuda_status(boba::launch_compact_window_assign(first, n, m_global, e0, m_local, all_counts, world, rank,
+                                                          label_partial, ws, ws_bytes, S(stream)),
+                       "boba_compact_shard_assign");
+}
+
+size_t boba_hub_table_bytes(void) { return boba::kHubTableBytes; }
+
+int boba_order_from_label(const uint32_t* label, uint32_t n, uint32_t* order, void* hubs, void* stream) {
+    REQUIRE((label && order) || n == 0, "boba_order_from_label: NULL argument");
+    return cuda_status(boba::launch_order_from_label(label, n, order, static_cast<unsigned long long*>(hubs),
+                                                     num_sms(), S(stream)),
+                       "boba_order_from_label");
+}
+
+int boba_relabel_hubs(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, const uint32_t* label,
+                      const void* hubs, uint32_t* I2, uint32_t* J2, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_relabel_hubs")) return rc;
+    REQUIRE((I && J && I2 && J2 && label) || m == 0, "boba_relabel_hubs: NULL argument");
+    return cuda_status(boba::launch_relabel(I, J, m, label, static_cast<const unsigned long long*>(hubs), I2, J2,
+                                            nullptr, n, num_sms(), S(stream)),
+                       "boba_relabel_hubs");
+}
+
+uint32_t boba_row_cut_buckets(uint32_t n) { return boba::row_cut_buckets(n); }
+
+int boba_row_cut_hist(const uint32_t* rows, uint64_t m_local, uint32_t n, uint32_t* hist, void* stream) {
+    REQUIRE(hist && (rows || m_local == 0), "boba_row_cut_hist: NULL argument");
+    return cuda_status(boba::launch_coarse_hist(rows, m_local, n, hist, num_sms(), S(stream)), "boba_row_cut_hist");
+}
+
+int boba_row_cut(const uint32_t* hist_global, const uint32_t* hist_local, uint32_t n, uint64_t m_global, int world,
+                 uint32_t* out, void* stream) {
+    REQUIRE(world >= 1 && world <= 256, "boba_row_cut: world must be in [1, 256]");
+    REQUIRE(m_global < 0xFFFFFFFFull, "boba_row_cut: m_global too large");
+    REQUIRE(hist_global && hist_local && out, "boba_row_cut: NULL argument");
+    return cuda_status(boba::launch_row_cut(hist_global, hist_local, n, m_global, world, out, S(stream)),
+                       "boba_row_cut");
 }
 
 int boba_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t count, uint32_t* out, void* stream) {

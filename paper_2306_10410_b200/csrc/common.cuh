@@ -4,6 +4,7 @@
 // offsets, radix bucket offsets and the SpMV row carries).
 #pragma once
 #include <atomic>
+#include <mutex>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -141,23 +142,31 @@ __device__ __forceinline__ unsigned long long warp_lookback_min(const unsigned l
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 // Kernel attributes (dynamic shared memory limit, carveout) belong to the
-// device's context: a call site sets them once per device, tracked here.
+// device's context: a call site sets them once per device, tracked here.  The
+// device's bit is set only after the attribute call succeeded, under a lock, so
+// a second host thread never launches before the attribute is in place and a
+// failed call is retried next time.
 struct PerDeviceOnce {
+    std::mutex mu;
     std::atomic<unsigned long long> done{0};
-    // true the first time it is asked on the current device (devices >= 64 always ask)
-    bool first() {
+    template <typename F>
+    cudaError_t run(F&& set) {
         int d = 0;
         cudaGetDevice(&d);
-        if (d >= 64) return true;
+        if (d >= 64) return set();  // devices >= 64: no cache, set every time
         const unsigned long long bit = 1ull << d;
-        return !(done.fetch_or(bit) & bit);
+        if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+        std::lock_guard<std::mutex> lock(mu);
+        if (done.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+        const cudaError_t e = set();
+        if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+        return e;
     }
 };
 
 template <typename K>
 inline cudaError_t set_attr_once(PerDeviceOnce& once, K* kernel, cudaFuncAttribute a, int v) {
-    if (!once.first()) return cudaSuccess;
-    return cudaFuncSetAttribute(kernel, a, v);
+    return once.run([&] { return cudaFuncSetAttribute(kernel, a, v); });
 }
 
 }  // namespace boba

@@ -243,4 +243,172 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
     return cudaGetLastError();
 }
 
+// ------------------------------------------------- sharded compaction ---
+// Multi-GPU phase 2 (sharded.py).  Rank r of P holds edges [e0, e0 + ml) of
+// the m-edge list, i.e. positions [e0, e0 + ml) of I and [m + e0, m + e0 + ml)
+// of J.  After the global first[] is known everywhere (allreduce-MIN), rank r
+// owns the vertices whose first position lies in one of its two windows and
+// compacts only those: a 2 ml-bit map over its windows (I window first), the
+// same record scan as above, and for every owned vertex its rank inside the
+// map.  The global rank follows from the 2P window counts (an allgather):
+// the scan order of [0, 2m) is I0 I1 .. I_{P-1} J0 J1 .. J_{P-1}, so
+//   I window of r: base = sum_{j<r} cI[j]
+//   J window of r: base = sum_j cI[j] + sum_{j<r} cJ[j] - cI[r]   (local rank counts cI[r] first)
+// Never-seen vertices get n_seen + their ascending rank, written by rank 0
+// only, so an allreduce-SUM of the per-rank partial labels (0 elsewhere) is
+// the global label array.  Reference semantics: _parallel.py:178-201.
+__device__ __forceinline__ bool window_pos(uint32_t f, uint64_t m, uint64_t e0, uint64_t ml, uint32_t& q) {
+    if (f == BOBA_UNSET) return false;
+    if ((uint64_t)f >= e0 && (uint64_t)f < e0 + ml) {
+        q = (uint32_t)(f - e0);
+        return true;
+    }
+    if ((uint64_t)f >= m + e0 && (uint64_t)f < m + e0 + ml) {
+        q = (uint32_t)(ml + (f - m - e0));
+        return true;
+    }
+    return false;
+}
+
+__global__ void k_mark_window(const uint32_t* __restrict__ first, uint32_t n, uint64_t m, uint64_t e0, uint64_t ml,
+                              uint32_t* recs) {
+    uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+        uint32_t q;
+        if (window_pos(__ldg(first + v), m, e0, ml, q)) {
+            const uint32_t w = q >> 5, r = rec_of_word(w);
+            atomicOr(recs + 8 * r + (w - r * kRecWords), 1u << (q & 31));
+        }
+    }
+}
+
+// counts[0] = owned vertices first seen in the I window, counts[1] = in the J window
+__global__ void k_window_counts(const uint4* __restrict__ recs, uint64_t ml, const uint32_t* __restrict__ n_seen,
+                                uint32_t* counts) {
+    const uint32_t ci = rank_of((uint32_t)ml, recs);
+    counts[0] = ci;
+    counts[1] = *n_seen - ci;
+}
+
+__global__ void __launch_bounds__(kScanNT) k_assign_window(const uint32_t* __restrict__ first, uint32_t n, uint64_t m,
+                                                           uint64_t e0, uint64_t ml, const uint4* __restrict__ recs,
+                                                           const uint32_t* __restrict__ all_counts, int world,
+                                                           int rank, uint32_t* label, unsigned long long* status,
+                                                           unsigned* tile_counter) {
+    __shared__ unsigned s_tile;
+    __shared__ uint32_t s_scan[kScanNT / 32 + 1];
+    __shared__ unsigned long long s_excl;
+    __shared__ uint32_t s_base[3];  // base_I, base_J, n_seen
+    if (threadIdx.x == 0) {
+        s_tile = atomicAdd(tile_counter, 1u);
+        uint32_t tot_i = 0, tot_j = 0, pre_i = 0, pre_j = 0;
+        for (int k = 0; k < world; k++) {
+            const uint32_t ci = all_counts[2 * k], cj = all_counts[2 * k + 1];
+            if (k < rank) pre_i += ci, pre_j += cj;
+            tot_i += ci, tot_j += cj;
+        }
+        s_base[0] = pre_i;
+        s_base[1] = tot_i + pre_j - all_counts[2 * rank];
+        s_base[2] = tot_i + tot_j;
+    }
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t v0 = tile * kAssignTile + (uint64_t)threadIdx.x * kAssignVPT;
+    uint32_t f[kAssignVPT];
+    uint32_t iso = 0;
+#pragma unroll
+    for (int k = 0; k < kAssignVPT; k++) {
+        f[k] = (v0 + k < n) ? __ldg(first + v0 + k) : 0u;
+        iso += (v0 + k < n && f[k] == BOBA_UNSET);
+    }
+    uint32_t total;
+    uint32_t iso_excl = block_exclusive_sum<kScanNT>(iso, s_scan, &total);
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0)
+            st_volatile_u64(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | (unsigned long long)total);
+        unsigned long long ex = tile == 0 ? 0ull : warp_lookback(status, (long long)tile);
+        if (threadIdx.x == 0) {
+            if (tile != 0) st_volatile_u64(status + tile, kFlagInc | (ex + total));
+            s_excl = ex;
+        }
+    }
+    __syncthreads();
+    uint32_t iso_rank = s_base[2] + (uint32_t)s_excl + iso_excl;
+    uint32_t lab[kAssignVPT];
+#pragma unroll
+    for (int k = 0; k < kAssignVPT; k++) {
+        uint32_t q, r = 0;
+        if (f[k] == BOBA_UNSET) {
+            r = rank == 0 ? iso_rank : 0u;
+            iso_rank++;
+        } else if (window_pos(f[k], m, e0, ml, q)) {
+            r = (q < ml ? s_base[0] : s_base[1]) + rank_of(q, recs);
+        }
+        lab[k] = r;
+    }
+    if (v0 + kAssignVPT <= n && (reinterpret_cast<uintptr_t>(label) & 15) == 0) {
+        *reinterpret_cast<uint4*>(label + v0) = make_uint4(lab[0], lab[1], lab[2], lab[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kAssignVPT; k++)
+            if (v0 + k < n) label[v0 + k] = lab[k];
+    }
+}
+
+__global__ void k_order_from_label(const uint32_t* __restrict__ label, uint32_t n, uint32_t* order) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) order[__ldg(label + v)] = v;
+}
+
+size_t compact_window_workspace_bytes(uint64_t ml, uint32_t n) { return carve_compact(nullptr, ml, n).total; }
+
+cudaError_t launch_compact_window_mark(const uint32_t* first, uint32_t n, uint64_t m, uint64_t e0, uint64_t ml,
+                                       uint32_t* counts, void* ws, size_t ws_bytes, int num_sms, cudaStream_t s) {
+    if (ws_bytes < compact_window_workspace_bytes(ml, n)) return cudaErrorInvalidValue;
+    CompactWs w = carve_compact(ws, ml, n);
+    const uint64_t nrec = num_recs(ml);
+    cudaError_t err = cudaMemsetAsync(ws, 0, w.total, s);
+    if (err != cudaSuccess) return err;
+    if (n) {
+        const uint64_t blocks = ceil_div(n, 256), cap = (uint64_t)num_sms * 16;
+        k_mark_window<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(first, n, m, e0, ml, w.recs);
+    }
+    k_rec_scan<<<(int)ceil_div(nrec, kRecsPerTile), kScanNT, 0, s>>>(reinterpret_cast<uint4*>(w.recs), nrec, w.st_rec,
+                                                                    w.counters + 0, w.counters + 4);
+    k_window_counts<<<1, 1, 0, s>>>(reinterpret_cast<const uint4*>(w.recs), ml, w.counters + 4, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compact_window_assign(const uint32_t* first, uint32_t n, uint64_t m, uint64_t e0, uint64_t ml,
+                                         const uint32_t* all_counts, int world, int rank, uint32_t* label, void* ws,
+                                         size_t ws_bytes, cudaStream_t s) {
+    if (ws_bytes < compact_window_workspace_bytes(ml, n)) return cudaErrorInvalidValue;
+    if (n == 0) return cudaSuccess;
+    CompactWs w = carve_compact(ws, ml, n);
+    cudaError_t err = cudaMemsetAsync(w.st_v, 0, (ceil_div((uint64_t)n, kAssignTile) + 1) * 8, s);
+    if (err == cudaSuccess) err = cudaMemsetAsync(w.counters + 1, 0, 4, s);
+    if (err != cudaSuccess) return err;
+    k_assign_window<<<(int)ceil_div((uint64_t)n, kAssignTile), kScanNT, 0, s>>>(
+        first, n, m, e0, ml, reinterpret_cast<const uint4*>(w.recs), all_counts, world, rank, label, w.st_v,
+        w.counters + 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_order_from_label(const uint32_t* label, uint32_t n, uint32_t* order,
+                                    unsigned long long* hubs, int num_sms, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t blocks = ceil_div(n, 256), cap = (uint64_t)num_sms * 16;
+    k_order_from_label<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(label, n, order);
+    if (hubs) {
+        cudaError_t err = cudaMemsetAsync(hubs, 0xFF, kHubTableBytes, s);
+        if (err != cudaSuccess) return err;
+        const HubHash hh = HubHash::make(n);
+        if (hh.tag_bits <= 16) {
+            const uint32_t K = n < kHubMaxLabel ? n : kHubMaxLabel;
+            k_hub_labels<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(order, K, hh, reinterpret_cast<uint32_t*>(hubs));
+        }
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace boba

@@ -416,10 +416,10 @@ size_t range_partition_workspace_bytes(uint64_t m, int parts) {
 
 cudaError_t launch_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds,
                                    int parts, uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out, void* ws,
-                                   size_t ws_bytes, int num_sms, cudaStream_t s) {
+                                   size_t ws_bytes, int num_sms, cudaStream_t s, bool relative) {
     if (parts < 1 || parts > 256) return cudaErrorInvalidValue;
     if (ws_bytes < range_partition_workspace_bytes(m, parts)) return cudaErrorInvalidValue;
-    if (m == 0) return cudaMemsetAsync(counts_out, 0, (size_t)parts * 4, s);
+    if (m == 0) return counts_out ? cudaMemsetAsync(counts_out, 0, (size_t)parts * 4, s) : cudaSuccess;
     const int bits = part_bits(parts);
     const uint64_t tiles = ceil_div(m, RadixCfg<8, 256, 16>::TILE);
     const uint64_t hcount = tiles << bits;
@@ -427,10 +427,10 @@ cudaError_t launch_range_partition(const uint32_t* keys, const uint32_t* vals, u
     uint32_t* H = reinterpret_cast<uint32_t*>(p);
     unsigned long long* st = reinterpret_cast<unsigned long long*>(p + (hcount * 4 + 255) / 256 * 256);
     unsigned* counter = reinterpret_cast<unsigned*>(st + ceil_div(hcount, kScanTile) + 1);
-    cudaError_t e = radix_pass_op<8, 256, 16, 4, DigitRange>(keys, vals, m, DigitRange{bounds, parts}, bits, H, st,
+    cudaError_t e = radix_pass_op<8, 256, 16, 4, DigitRange>(keys, vals, m, DigitRange{bounds, parts, relative}, bits, H, st,
                                                              counter, keys_out, vals_out, num_sms, s);
     if (e != cudaSuccess) return e;
-    k_part_counts<<<1, 256, 0, s>>>(H, tiles, parts, m, counts_out);
+    if (counts_out) k_part_counts<<<1, 256, 0, s>>>(H, tiles, parts, m, counts_out);
     return cudaGetLastError();
 }
 

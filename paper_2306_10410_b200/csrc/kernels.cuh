@@ -56,7 +56,7 @@ cudaError_t launch_offset_ids(const uint32_t* in, uint64_t count, uint32_t delta
 size_t range_partition_workspace_bytes(uint64_t m, int parts);
 cudaError_t launch_range_partition(const uint32_t* keys, const uint32_t* vals, uint64_t m, const uint32_t* bounds,
                                    int parts, uint32_t* keys_out, uint32_t* vals_out, uint32_t* counts_out, void* ws,
-                                   size_t ws_bytes, int num_sms, cudaStream_t s);
+                                   size_t ws_bytes, int num_sms, cudaStream_t s, bool relative = false);
 cudaError_t launch_iota(uint32_t* out, uint64_t count, int num_sms, cudaStream_t s);
 size_t sort_pairs_workspace_bytes(uint64_t count, int key_bits);
 cudaError_t launch_sort_pairs(const uint32_t* keys, const uint32_t* vals, uint64_t count, int key_bits,
@@ -86,12 +86,24 @@ size_t nbr_workspace_bytes(uint64_t m, uint32_t n);
 cudaError_t launch_nbr(const uint32_t* offsets, const uint32_t* indices, uint32_t n, uint64_t m, uint32_t line_size,
                        double* out, void* ws, size_t ws_bytes, int num_sms, cudaStream_t s);
 
-// multi-GPU row-partitioned CSR (shard.cu)
-cudaError_t launch_adjacent_diff(const uint32_t* in, uint64_t count, uint32_t* out, int num_sms, cudaStream_t s);
-size_t merge_rows_workspace_bytes(int parts, uint32_t rows, uint64_t recv_len);
-// recv_len must equal the sum of counts
-cudaError_t launch_merge_rows(const uint32_t* recv, uint64_t recv_len, int parts, uint32_t rows,
-                              const uint32_t* counts, const uint32_t* out_off, uint32_t* out, void* ws,
-                              size_t ws_bytes, int num_sms, cudaStream_t s);
+// multi-GPU (sharded.py): windowed compaction (compact.cu) and the row cut (shard.cu)
+size_t compact_window_workspace_bytes(uint64_t ml, uint32_t n);
+cudaError_t launch_compact_window_mark(const uint32_t* first, uint32_t n, uint64_t m, uint64_t e0, uint64_t ml,
+                                       uint32_t* counts, void* ws, size_t ws_bytes, int num_sms, cudaStream_t s);
+cudaError_t launch_compact_window_assign(const uint32_t* first, uint32_t n, uint64_t m, uint64_t e0, uint64_t ml,
+                                         const uint32_t* all_counts, int world, int rank, uint32_t* label, void* ws,
+                                         size_t ws_bytes, cudaStream_t s);
+cudaError_t launch_order_from_label(const uint32_t* label, uint32_t n, uint32_t* order, unsigned long long* hubs,
+                                    int num_sms, cudaStream_t s);
+uint32_t row_cut_buckets(uint32_t n);
+cudaError_t launch_coarse_hist(const uint32_t* rows, uint64_t m, uint32_t n, uint32_t* hist, int num_sms,
+                               cudaStream_t s);
+cudaError_t launch_row_cut(const uint32_t* hist_g, const uint32_t* hist_l, uint32_t n, uint64_t m, int parts,
+                           uint32_t* out, cudaStream_t s);
+
+// host <-> device id transfers through pinned staging (hostio.cu); synchronous
+cudaError_t host_h2d_ids(const int64_t* host, uint64_t count, uint64_t bound, uint32_t* dev, int64_t* bad,
+                         cudaStream_t s);
+cudaError_t host_d2h_ids(const uint32_t* dev, uint64_t count, int64_t* host, cudaStream_t s);
 
 }  // namespace boba

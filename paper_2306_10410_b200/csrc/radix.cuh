@@ -30,14 +30,19 @@ struct DigitShift {
     int shift;
     uint32_t mask;
     __device__ __forceinline__ uint32_t operator()(uint32_t k) const { return (k >> shift) & mask; }
+    __device__ __forceinline__ uint32_t out_key(uint32_t k, uint32_t) const { return k; }
 };
 struct DigitRange {
     const uint32_t* bounds;  // parts + 1 ascending row boundaries (device)
     int parts;
+    bool relative;           // keys written relative to their part's first row
     __device__ __forceinline__ uint32_t operator()(uint32_t k) const {
         uint32_t o = 0;
         for (int p = 1; p < parts; p++) o += k >= __ldg(bounds + p);
         return o;
+    }
+    __device__ __forceinline__ uint32_t out_key(uint32_t k, uint32_t d) const {
+        return relative ? k - __ldg(bounds + d) : k;
     }
 };
 
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
         const uint2 kv = s_kv[kv_swz(j)];
         const uint32_t d = op(kv.x);
         const uint32_t g = s_glob[d] + (uint32_t)j;
-        if (keys_out) keys_out[g] = kv.x;
+        if (keys_out) keys_out[g] = op.out_key(kv.x, d);
         vals_out[g] = kv.y;
         if (row_starts) {
             // Last (most significant) pass: the output is sorted by key, and this

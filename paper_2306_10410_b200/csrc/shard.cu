@@ -1,151 +1,145 @@
-// Multi-GPU helpers for the row-partitioned CSR (paper_2306_10410_b200/sharded.py).
+// Multi-GPU row cut for the row-partitioned CSR (paper_2306_10410_b200/sharded.py).
 //
-// Each rank sorts its contiguous edge shard into a local CSR over all n rows
-// (the same stable radix COO->CSR as one GPU), so the edges a rank must send
-// to the owner of rows [b_k, b_k+1) are one contiguous run of its local
-// indices, already in row order and, within a row, in shard order.  The owner
-// receives one such run per sender (in rank order) plus each sender's
-// per-row counts, and interleaves them row by row: row r = sender 0's
-// entries, then sender 1's, ...  Shards are contiguous in edge order, so that
-// is global edge order -- the reference's within-row order
-// (_parallel.py:55-88) -- and the CSR is bit-exact.
+// After relabel, rank r holds the relabelled edges of its contiguous shard.
+// The CSR rows are split into P contiguous row ranges of ~m/P edges each,
+// owned by ranks 0..P-1.  Choosing the cut needs the global row histogram;
+// an n-sized allreduce of it (268 MB at s26) is avoided with a coarse one:
+//
+//   k_coarse_hist  histogram of rows >> shift over B <= 32768 buckets, in
+//                  shared memory per CTA, flushed with one atomic per bucket;
+//   (allreduce-SUM of the B-word histogram -- 128 KB)
+//   k_row_cut      one CTA: prefix sums of the global and the local coarse
+//                  histograms; cut k is the first bucket boundary whose global
+//                  prefix reaches k*m/P.  Writes the row bounds, each owner's
+//                  first global edge offset and this rank's send counts (the
+//                  local prefix at the bounds -- exact, since bounds sit on
+//                  bucket boundaries).
+//
+// The send side is then one stable range partition (csr.cu, keys written
+// relative to the owner's first row), the exchange an all-to-all, and the
+// owner's CSR the one-GPU stable COO->CSR of what it received: senders are
+// ranks in order and shards are contiguous in edge order, so the received
+// sequence is global edge order restricted to the owner's rows -- the
+// reference's within-row order (_parallel.py:55-88), bit-exact.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace boba {
 
-__global__ void k_adjacent_diff(const uint32_t* __restrict__ in, uint64_t count, uint32_t* out) {
+constexpr uint32_t kCutMaxBuckets = 32768;
+constexpr int kCutNT = 1024;
+
+int row_cut_shift(uint32_t n) {
+    const int bits = n <= 1 ? 0 : 32 - __builtin_clz(n - 1);
+    return bits > 15 ? bits - 15 : 0;
+}
+
+uint32_t row_cut_buckets(uint32_t n) {
+    const int sh = row_cut_shift(n);
+    return n == 0 ? 1u : (uint32_t)(((uint64_t)n + (1ull << sh) - 1) >> sh);
+}
+
+__global__ void k_coarse_hist(const uint32_t* __restrict__ rows, uint64_t m, int shift, uint32_t B,
+                              uint32_t* __restrict__ hist) {
+    extern __shared__ uint32_t s_h[];
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) s_h[b] = 0;
+    __syncthreads();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
-        out[i] = __ldg(in + i + 1) - __ldg(in + i);
-}
-
-// Segment s = k * rows + r is sender k's run for row r: it starts at
-// src_start[s] in recv (rank-major exclusive scan of the counts) and goes to
-// dst[s] = out_off[r] + (entries of senders < k in row r) in the output.
-__global__ void k_merge_dst(const uint32_t* __restrict__ counts, int parts, uint32_t rows,
-                            const uint32_t* __restrict__ out_off, uint32_t* __restrict__ dst) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
-        uint32_t d = __ldg(out_off + r);
-        for (int k = 0; k < parts; k++) {
-            dst[(uint64_t)k * rows + r] = d;
-            d += __ldg(counts + (uint64_t)k * rows + r);
-        }
+    const uint64_t quads = (reinterpret_cast<uintptr_t>(rows) & 15) == 0 ? m >> 2 : 0;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += stride) {
+        const uint4 r = __ldg(reinterpret_cast<const uint4*>(rows) + q);
+        atomicAdd(s_h + (r.x >> shift), 1u);
+        atomicAdd(s_h + (r.y >> shift), 1u);
+        atomicAdd(s_h + (r.z >> shift), 1u);
+        atomicAdd(s_h + (r.w >> shift), 1u);
     }
+    for (uint64_t e = 4 * quads + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride)
+        atomicAdd(s_h + (__ldg(rows + e) >> shift), 1u);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x)
+        if (s_h[b]) atomicAdd(hist + b, s_h[b]);
 }
 
-// Item-balanced copy: each CTA moves kMcTile consecutive recv entries.  The
-// segments it spans are located once per CTA (binary search over src_start)
-// and their (start, dst) pairs staged in shared memory; each entry then finds
-// its segment by a search in shared memory (in global memory if the chunk
-// spans more than kMcSegs segments, i.e. runs of empty rows).
-constexpr int kMcNT = 256, kMcIPT = 8, kMcTile = kMcNT * kMcIPT, kMcSegs = 4096;
-
-__device__ __forceinline__ uint64_t seg_of(const uint32_t* a, uint64_t lo, uint64_t hi, uint32_t p) {
-    // last index i in [lo, hi) with a[i] <= p (a[lo] <= p assumed)
-    while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (a[mid] <= p) lo = mid; else hi = mid;
+// out (3P + 2 words): [0, P]      row bounds b_0 = 0 <= ... <= b_P = n
+//                     [P+1, 2P+1] global edge offset of each bound (offsets[b_k])
+//                     [2P+2, 3P+1] edges this rank sends to owner k
+__global__ void __launch_bounds__(kCutNT) k_row_cut(const uint32_t* __restrict__ hist_g,
+                                                    const uint32_t* __restrict__ hist_l, uint32_t B, int shift,
+                                                    uint32_t n, uint64_t m, int P, uint32_t* __restrict__ out) {
+    constexpr int kPer = kCutMaxBuckets / kCutNT;  // 32 buckets per thread
+    __shared__ unsigned long long s_g[kCutNT], s_l[kCutNT];
+    __shared__ unsigned long long s_cut_l[257];
+    const uint32_t b0 = threadIdx.x * kPer;
+    unsigned long long g = 0, l = 0;
+    for (int i = 0; i < kPer; i++)
+        if (b0 + i < B) g += hist_g[b0 + i], l += hist_l[b0 + i];
+    s_g[threadIdx.x] = g;
+    s_l[threadIdx.x] = l;
+    __syncthreads();
+    // exclusive prefix of the per-thread sums (Hillis-Steele in shared memory, 1024 entries)
+    for (int o = 1; o < kCutNT; o <<= 1) {
+        unsigned long long a = threadIdx.x >= (unsigned)o ? s_g[threadIdx.x - o] : 0ull;
+        unsigned long long c = threadIdx.x >= (unsigned)o ? s_l[threadIdx.x - o] : 0ull;
+        __syncthreads();
+        s_g[threadIdx.x] += a;
+        s_l[threadIdx.x] += c;
+        __syncthreads();
     }
-    return lo;
-}
-
-// Segments of every chunk's first and last entry, all chunks in parallel (a
-// serial search per CTA would sit on the critical path of every chunk).
-__global__ void k_merge_partition(const uint32_t* __restrict__ src_start, uint64_t nseg, uint64_t total,
-                                  uint64_t chunks, uint64_t* __restrict__ seg_range) {
-    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= chunks) return;
-    const uint64_t p0 = c * kMcTile, p1 = p0 + kMcTile < total ? p0 + kMcTile : total;
-    seg_range[2 * c] = seg_of(src_start, 0, nseg + 1, (uint32_t)p0);
-    seg_range[2 * c + 1] = seg_of(src_start, 0, nseg + 1, (uint32_t)(p1 - 1));
-}
-
-__global__ void __launch_bounds__(kMcNT) k_merge_copy(const uint32_t* __restrict__ recv, uint64_t total,
-                                                      const uint32_t* __restrict__ src_start,
-                                                      const uint32_t* __restrict__ dst,
-                                                      const uint64_t* __restrict__ seg_range,
-                                                      uint32_t* __restrict__ out) {
-    __shared__ uint32_t s_start[kMcSegs + 1];
-    __shared__ uint32_t s_dst[kMcSegs];
-    const uint64_t p0 = (uint64_t)blockIdx.x * kMcTile;
-    const uint64_t p1 = p0 + kMcTile < total ? p0 + kMcTile : total;
-    const uint64_t sa = __ldg(seg_range + 2 * blockIdx.x), sb = __ldg(seg_range + 2 * blockIdx.x + 1);
-    const bool staged = sb - sa < (uint64_t)kMcSegs;
-    if (staged) {
-        for (uint64_t i = threadIdx.x; i <= sb - sa; i += kMcNT) {
-            s_start[i] = __ldg(src_start + sa + i);
-            s_dst[i] = __ldg(dst + sa + i);
+    unsigned long long G = s_g[threadIdx.x] - g, L = s_l[threadIdx.x] - l;  // prefixes at b0
+    // bucket boundary b (0..B) with prefix G_b: cut k is the smallest b with G_b >= k*m/P
+    for (int i = 0; i <= kPer; i++) {
+        const uint32_t b = b0 + i;
+        if (b > B || (i == kPer && b != B)) break;   // boundary B is checked by its owner only
+        const unsigned long long Gprev = G;          // G_b
+        for (int k = 1; k < P; k++) {
+            const unsigned long long t = (unsigned long long)k * m / (unsigned long long)P;
+            // first b with G_b >= t: G_b >= t and (b == 0 or G_{b-1} < t); G_{b-1} = G_b - hist_g[b-1]
+            const unsigned long long before = b == 0 ? 0ull : Gprev - hist_g[b - 1];
+            if (Gprev >= t && (b == 0 || before < t)) {
+                const uint64_t row = (uint64_t)b << shift;
+                out[k] = (uint32_t)(row < n ? row : n);
+                out[P + 1 + k] = (uint32_t)Gprev;
+                s_cut_l[k] = L;
+            }
         }
-        if (threadIdx.x == 0) s_start[sb - sa + 1] = __ldg(src_start + sb + 1);
+        if (b < B) {
+            G += hist_g[b];
+            L += hist_l[b];
+        }
     }
     __syncthreads();
-    // each warp: 256 consecutive entries, lane-interleaved (coalesced loads and
-    // stores); its segment range is found once, then each entry searches it
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    const uint64_t w0 = p0 + (uint64_t)warp * 32 * kMcIPT;
-    if (w0 >= p1) return;
-    const uint64_t w1 = w0 + 32 * kMcIPT < p1 ? w0 + 32 * kMcIPT : p1;
-    if (staged) {
-        const uint32_t nst = (uint32_t)(sb - sa + 1);
-        const uint32_t lo = (uint32_t)seg_of(s_start, 0, nst + 1, (uint32_t)w0);
-        const uint32_t hi = (uint32_t)seg_of(s_start, lo, nst + 1, (uint32_t)(w1 - 1)) + 1;
-#pragma unroll
-        for (int u = 0; u < kMcIPT; u++) {
-            const uint64_t p = w0 + (uint64_t)u * 32 + lane;
-            if (p < w1) {
-                const uint32_t i = (uint32_t)seg_of(s_start, lo, hi, (uint32_t)p);
-                out[s_dst[i] + ((uint32_t)p - s_start[i])] = __ldg(recv + p);
-            }
-        }
-    } else {
-#pragma unroll
-        for (int u = 0; u < kMcIPT; u++) {
-            const uint64_t p = w0 + (uint64_t)u * 32 + lane;
-            if (p < w1) {
-                const uint64_t i = seg_of(src_start, sa, sb + 2, (uint32_t)p);
-                out[__ldg(dst + i) + ((uint32_t)p - __ldg(src_start + i))] = __ldg(recv + p);
-            }
-        }
+    if (threadIdx.x == 0) {
+        out[0] = 0;
+        out[P] = n;
+        out[P + 1] = 0;
+        out[2 * P + 1] = (uint32_t)m;
+        s_cut_l[0] = 0;
+        s_cut_l[P] = s_l[kCutNT - 1];  // inclusive total of the local histogram
+        for (int k = 0; k < P; k++) out[2 * P + 2 + k] = (uint32_t)(s_cut_l[k + 1] - s_cut_l[k]);
     }
 }
 
-cudaError_t launch_adjacent_diff(const uint32_t* in, uint64_t count, uint32_t* out, int num_sms, cudaStream_t s) {
-    if (count == 0) return cudaSuccess;
-    const uint64_t blocks = ceil_div(count, 256), cap = (uint64_t)num_sms * 8;
-    k_adjacent_diff<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(in, count, out);
+cudaError_t launch_coarse_hist(const uint32_t* rows, uint64_t m, uint32_t n, uint32_t* hist, int num_sms,
+                               cudaStream_t s) {
+    const uint32_t B = row_cut_buckets(n);
+    cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)B * 4, s);
+    if (e != cudaSuccess || m == 0) return e;
+    static PerDeviceOnce attr;
+    const int smem = (int)(B * 4);
+    if (smem > 48 * 1024) {
+        e = set_attr_once(attr, k_coarse_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kCutMaxBuckets * 4));
+        if (e != cudaSuccess) return e;
+    }
+    const uint64_t blocks = ceil_div(m, 4 * 512);
+    const int grid = (int)(blocks < (uint64_t)num_sms ? blocks : (uint64_t)num_sms);
+    k_coarse_hist<<<grid, 512, smem, s>>>(rows, m, row_cut_shift(n), B, hist);
     return cudaGetLastError();
 }
 
-size_t merge_rows_workspace_bytes(int parts, uint32_t rows, uint64_t recv_len) {
-    const uint64_t cnt = (uint64_t)parts * rows;
-    return 2 * (((cnt + 1) * 4 + 255) / 256 * 256) + (ceil_div(cnt + 1, 2048) + 2) * 8 + 256 +
-           (ceil_div(recv_len, kMcTile) + 1) * 16;
-}
-
-cudaError_t launch_merge_rows(const uint32_t* recv, uint64_t recv_len, int parts, uint32_t rows,
-                              const uint32_t* counts, const uint32_t* out_off, uint32_t* out, void* ws,
-                              size_t ws_bytes, int num_sms, cudaStream_t s) {
-    if (ws_bytes < merge_rows_workspace_bytes(parts, rows, recv_len)) return cudaErrorInvalidValue;
-    if (rows == 0 || parts == 0) return cudaSuccess;
-    const uint64_t cnt = (uint64_t)parts * rows;
-    const size_t arr = ((cnt + 1) * 4 + 255) / 256 * 256;
-    char* p = static_cast<char*>(ws);
-    uint32_t* src_start = reinterpret_cast<uint32_t*>(p);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(p + arr);
-    unsigned long long* st = reinterpret_cast<unsigned long long*>(p + 2 * arr);
-    unsigned* counter = reinterpret_cast<unsigned*>(st + ceil_div(cnt + 1, 2048) + 1);
-    // rank-major exclusive scan of the counts = segment starts in recv (senders' runs back to back)
-    cudaError_t e = launch_row_offsets(counts, (uint32_t)cnt, src_start, st, counter, s);
-    if (e != cudaSuccess) return e;
-    const uint64_t rb = ceil_div(rows, 256), cap = (uint64_t)num_sms * 8;
-    k_merge_dst<<<(unsigned)(rb < cap ? rb : cap), 256, 0, s>>>(counts, parts, rows, out_off, dst);
-    if (recv_len == 0) return cudaGetLastError();
-    const uint64_t chunks = ceil_div(recv_len, kMcTile);
-    uint64_t* seg_range = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(counter) + 256);
-    k_merge_partition<<<(unsigned)ceil_div(chunks, 256), 256, 0, s>>>(src_start, cnt, recv_len, chunks, seg_range);
-    k_merge_copy<<<(unsigned)chunks, kMcNT, 0, s>>>(recv, recv_len, src_start, dst, seg_range, out);
+cudaError_t launch_row_cut(const uint32_t* hist_g, const uint32_t* hist_l, uint32_t n, uint64_t m, int parts,
+                           uint32_t* out, cudaStream_t s) {
+    if (parts < 1 || parts > 256) return cudaErrorInvalidValue;
+    k_row_cut<<<1, kCutNT, 0, s>>>(hist_g, hist_l, row_cut_buckets(n), row_cut_shift(n), n, m, parts, out);
     return cudaGetLastError();
 }
 

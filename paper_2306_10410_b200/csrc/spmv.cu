@@ -120,6 +120,15 @@ __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restr
     const uint32_t items_tile = (uint32_t)((d0 + kSpTile < total ? d0 + kSpTile : total) - d0);
     const uint32_t i0 = __ldg(coords + tile), i1 = __ldg(coords + tile + 1);
     const uint64_t j0 = d0 - i0;
+    // A reused partition (reuse_partition = 1) that does not belong to this
+    // CSR could hold any coords: never index s_end / s_val past the tile.
+    if (i1 < i0 || i1 - i0 > items_tile || i1 > n) {
+        if (gt == 0) {
+            tile_head[tile] = 0xFFFFFFFFu;
+            tile_tail[tile] = T(0);
+        }
+        return;
+    }
     const uint32_t nrows = i1 - i0, nnz = items_tile - nrows;
     const uint32_t j0_32 = (uint32_t)j0;  // offsets are uint32: relative ends are exact mod 2^32
     for (uint32_t k = gt; k <= nrows; k += kSpNT)

@@ -247,6 +247,12 @@ class CapturedPipeline:
         N.check(N.lib.boba_graph_launch(self._g, _s()))
         return self.pipe
 
+    def kernel_nodes(self) -> int:
+        """Kernel launches one replay performs."""
+        k = ctypes.c_uint64()
+        N.check(N.lib.boba_graph_kernel_nodes(self._g, ctypes.byref(k)))
+        return int(k.value)
+
     def close(self):
         if self._g:
             N.lib.boba_reorder_to_csr_graph_destroy(self._g)

@@ -1,27 +1,36 @@
 """Multi-GPU BOBA pipeline over contiguous edge shards.
 
-One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  Rank k
-holds edges [e0_k, e0_k + m_k) of the global edge list, in order:
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  Rank r
+of P holds edges [e0, e0 + ml) of the m-edge list, in order, i.e. positions
+[e0, e0 + ml) of I and [m + e0, m + e0 + ml) of J:
 
   P1  local first occurrence with global positions
       (boba_first_occurrence_shard), then an allreduce-MIN of the n-sized
       array -- the reference's exact chunk-local-min merge
       (_parallel.py:139-162).  uint32 positions are mapped to int32 with the
-      order-preserving bias x ^ 0x80000000 so a signed MIN collective is exact
-      (UNSET = 0xFFFFFFFF stays the largest, position 2^31-1 stays distinct).
-  P2  rank compaction, replicated on every rank (O(n + m/32) work, no
-      communication): order and label are identical everywhere.
-  P3  relabel of the local shard against the replicated label.
-  P4  each rank builds the stable CSR of its shard over all n rows (the
-      one-GPU COO->CSR); the sum of the local offsets arrays (allreduce-SUM)
-      is the global offsets array.  Rows are cut into P ranges of ~m/P edges.
-      The edges rank j owes the owner of rows [b_k, b_k+1) are one contiguous
-      run of its local indices, so one all-to-all of column ids (4 bytes per
-      edge) and one of per-row counts deliver them; the owner interleaves the
-      runs row by row in rank order (boba_merge_rows).  Shards are contiguous
-      in edge order, so that is global edge order: the reference's
-      within-row order, bit-exact.
-  P5  row-partitioned SpMV; x replicated (allgather of y slices to iterate).
+      order-preserving bias x ^ 0x80000000 so a signed MIN collective is exact.
+  P2  compaction split by position window (_parallel.py:178-201): each rank
+      ranks only the vertices first seen in its two windows
+      (boba_compact_shard_mark / _assign); the global rank adds a prefix over
+      the 2P window counts (allgather of 2 words per rank).  The partial
+      label arrays (one owner per vertex, 0 elsewhere) are merged by an
+      allreduce-SUM; order = inverse of label, built locally.
+  P3  relabel of the local shard against the replicated label, with the hub
+      label table (graph.py:280-289).
+  P4  row-partitioned CSR (graph.py:253-277): a coarse row histogram
+      (<= 32768 buckets, allreduce-SUM of 128 KB) fixes P edge-balanced row
+      ranges on bucket boundaries and every rank's send counts; one stable
+      range partition of (row, col) per rank, an all-to-all of rows and of
+      cols, and the owner's stable COO->CSR of what it received.  Senders are
+      ranks in order and shards are contiguous in edge order, so the received
+      sequence is global edge order restricted to the owner's rows: the
+      reference's within-row order (_parallel.py:55-88), bit-exact.
+  P5  row-partitioned SpMV (kernels.py:30-52): the owner multiplies its rows
+      by the replicated x; between iterations every owner broadcasts its y
+      slice (an allgather-v) into the next x.
+
+Host synchronisations per step: one (the 3P + 2 + P words of row bounds and
+send / receive counts the all-to-all needs on the host).
 
 The algorithm is written against a small ``ops`` object (DeviceOps below:
 the C ABI on CUDA tensors).  The multi-process CPU tests substitute a numpy
@@ -42,12 +51,16 @@ from . import device as D
 _MIN, _SUM = dist.ReduceOp.MIN, dist.ReduceOp.SUM
 
 
+def _e(k, dev):
+    return torch.empty(max(k, 1), dtype=D.ID, device=dev)[:k]
+
+
 class DeviceOps:
     """Local phases on the current CUDA device (uint32 ids in int32 storage)."""
 
     def first_occurrence_shard(self, I, J, m_global: int, e0: int, n: int):
-        first = torch.empty(max(n, 1), dtype=D.ID, device=I.device)[:n]
-        ws = D._ws(N.lib.boba_first_occurrence_workspace_size(), I.device)
+        first = _e(n, I.device)
+        ws = D._ws(N.lib.boba_first_occurrence_shard_workspace_size(n), I.device)
         N.check(N.lib.boba_first_occurrence_shard(D._p(I), D._p(J), I.numel(), m_global, e0, n, D._p(first), 0,
                                                   D._p(ws), ws.numel(), D._s()))
         return first
@@ -57,63 +70,60 @@ class DeviceOps:
         N.check(N.lib.boba_bias_u32(D._p(t), t.numel(), D._p(out), D._s()))
         return out
 
-    def compact(self, first, m_global: int, n: int):
-        return D.compact(first, m_global, n)
+    def compact_shard_mark(self, first, n: int, m_global: int, e0: int, ml: int):
+        """-> (counts[2], workspace to pass to compact_shard_assign)."""
+        ws = D._ws(N.lib.boba_compact_shard_workspace_size(ml, n), first.device)
+        counts = _e(2, first.device)
+        N.check(N.lib.boba_compact_shard_mark(D._p(first), n, m_global, e0, ml, D._p(counts), D._p(ws), ws.numel(),
+                                              D._s()))
+        return counts, ws
 
-    def relabel(self, I, J, label, n: int):
-        return D.relabel(I, J, label, n)
+    def compact_shard_assign(self, first, n: int, m_global: int, e0: int, ml: int, all_counts, world: int,
+                             rank: int, ws):
+        label = _e(n, first.device)
+        N.check(N.lib.boba_compact_shard_assign(D._p(first), n, m_global, e0, ml, D._p(all_counts), world, rank,
+                                                D._p(label), D._p(ws), ws.numel(), D._s()))
+        return label
 
-    def compact_relabel(self, first, I, J, m_global: int, n: int):
-        """P2 + P3 with the hub label table, as in the fused one-GPU call."""
-        dev = I.device
+    def order_from_label(self, label, n: int):
+        """-> (order, hub label table for relabel)."""
+        order = _e(n, label.device)
+        hubs = D._ws(N.lib.boba_hub_table_bytes(), label.device)
+        N.check(N.lib.boba_order_from_label(D._p(label), n, D._p(order), D._p(hubs), D._s()))
+        return order, hubs
+
+    def relabel(self, I, J, label, hubs, n: int):
         m = I.numel()
-        e = lambda k: torch.empty(max(k, 1), dtype=D.ID, device=dev)[:k]  # noqa: E731
-        order, label, I2, J2 = e(n), e(n), e(m), e(m)
-        ws = D._ws(N.lib.boba_compact_relabel_workspace_size(m_global, n), dev)
-        N.check(N.lib.boba_compact_relabel(D._p(first), m_global, n, D._p(I), D._p(J), m, D._p(order), D._p(label),
-                                           D._p(I2), D._p(J2), D._p(ws), ws.numel(), D._s()))
-        return order, label, I2, J2
+        I2, J2 = _e(m, I.device), _e(m, I.device)
+        N.check(N.lib.boba_relabel_hubs(D._p(I), D._p(J), m, n, D._p(label), D._p(hubs), D._p(I2), D._p(J2),
+                                        D._s()))
+        return I2, J2
 
-    def degrees(self, I2, n: int):
-        return D.degrees(I2, n)
+    def row_cut_hist(self, rows, n: int):
+        hist = _e(int(N.lib.boba_row_cut_buckets(n)), rows.device)
+        N.check(N.lib.boba_row_cut_hist(D._p(rows), rows.numel(), n, D._p(hist), D._s()))
+        return hist
 
-    def exclusive_scan(self, counts):
-        n = counts.numel()
-        out = torch.empty(n + 1, dtype=D.ID, device=counts.device)
-        ws = D._ws(N.lib.boba_exclusive_scan_workspace_size(n), counts.device)
-        N.check(N.lib.boba_exclusive_scan_u32(D._p(counts), n, D._p(out), D._p(ws), ws.numel(), D._s()))
+    def row_cut(self, hist_g, hist_l, n: int, m_global: int, parts: int):
+        out = _e(3 * parts + 2, hist_g.device)
+        N.check(N.lib.boba_row_cut(D._p(hist_g), D._p(hist_l), n, m_global, parts, D._p(out), D._s()))
         return out
 
     def range_partition(self, keys, vals, bounds, parts: int):
+        """Stable partition by row range, keys written relative to their part."""
         m = keys.numel()
         ko, vo = torch.empty_like(keys), torch.empty_like(vals)
-        counts = torch.empty(parts, dtype=D.ID, device=keys.device)
         ws = D._ws(N.lib.boba_range_partition_workspace_size(m, parts), keys.device)
-        N.check(N.lib.boba_range_partition(D._p(keys), D._p(vals), m, D._p(bounds), parts, D._p(ko), D._p(vo),
-                                           D._p(counts), D._p(ws), ws.numel(), D._s()))
-        return ko, vo, counts
-
-    def offset_ids(self, t, delta: int):
-        out = torch.empty_like(t)
-        N.check(N.lib.boba_offset_ids(D._p(t), t.numel(), delta & 0xFFFFFFFF, D._p(out), D._s()))
-        return out
+        N.check(N.lib.boba_range_partition_ex(D._p(keys), D._p(vals), m, D._p(bounds), parts, 1, D._p(ko), D._p(vo),
+                                              None, D._p(ws), ws.numel(), D._s()))
+        return ko, vo
 
     def coo_to_csr(self, rows, cols, n_rows: int):
         offsets, indices, _ = D.coo_to_csr(rows, cols, n_rows)
         return offsets, indices
 
-    def adjacent_diff(self, t):
-        out = torch.empty(max(t.numel() - 1, 1), dtype=D.ID, device=t.device)[: t.numel() - 1]
-        N.check(N.lib.boba_adjacent_diff_u32(D._p(t), t.numel() - 1, D._p(out), D._s()))
-        return out
-
-    def merge_rows(self, recv, counts, parts: int, rows: int, out_offsets):
-        total = recv.numel()
-        out = torch.empty(max(total, 1), dtype=D.ID, device=recv.device)[:total]
-        ws = D._ws(N.lib.boba_merge_rows_workspace_size(parts, rows, total), recv.device)
-        N.check(N.lib.boba_merge_rows(D._p(recv), total, parts, rows, D._p(counts), D._p(out_offsets), D._p(out),
-                                      D._p(ws), ws.numel(), D._s()))
-        return out
+    def spmv(self, offsets, indices, x, out):
+        return D.spmv(offsets, indices, x, out=out)
 
 
 @dataclass
@@ -127,23 +137,10 @@ class ShardResult:
     row_hi: int
     offsets: torch.Tensor     # local CSR offsets (row_hi - row_lo + 1), relative to the local indices
     indices: torch.Tensor     # column ids (global labels)
-    global_offsets: torch.Tensor  # n + 1, replicated
-
-
-def row_bounds(offsets_g: torch.Tensor, m_global: int, parts: int) -> torch.Tensor:
-    """Cut rows so that part k starts at the first row whose global offset is
-    >= k * m / parts (edge-balanced ranges; a part may be empty)."""
-    n = offsets_g.numel() - 1
-    targets = torch.tensor([(k * m_global) // parts for k in range(1, parts)], dtype=torch.int64,
-                           device=offsets_g.device)
-    offs = offsets_g.to(torch.int64) & 0xFFFFFFFF
-    cut = torch.searchsorted(offs, targets, side="left").clamp_(0, n)
-    b = torch.empty(parts + 1, dtype=torch.int64, device=offsets_g.device)
-    b[0], b[parts] = 0, n
-    if parts > 1:
-        b[1:parts] = cut
-        b = torch.cummax(b, 0).values  # monotone even with empty parts
-    return b
+    row_edge_offset: int      # global offsets[row_lo]: the global CSR offsets are offsets + row_edge_offset
+    bounds: list              # all owners' row bounds b_0 = 0 <= ... <= b_P = n
+    sent: list                # edges this rank sent to each owner
+    received: list            # edges this rank received from each sender
 
 
 def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int], group=None) -> torch.Tensor:
@@ -153,42 +150,77 @@ def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int
 
 
 def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: int, e0: int, group=None,
-                           ops=None) -> ShardResult:
-    """Run the BOBA pipeline on this rank's contiguous shard (see module doc)."""
+                           ops=None, mark=None) -> ShardResult:
+    """Run the BOBA pipeline on this rank's contiguous shard (see module doc).
+    `mark(name)`, if given, is called at every phase boundary (timing)."""
     ops = ops or DeviceOps()
+    mark = mark or (lambda name: None)
     P = dist.get_world_size(group)
     r = dist.get_rank(group)
+    ml = I.numel()
+    mark("start")
     # P1: local first occurrence, exact global merge
     first = ops.first_occurrence_shard(I, J, m_global, e0, n)
     key = ops.bias(first)
     dist.all_reduce(key, op=_MIN, group=group)
     first = ops.bias(key)
-    # P2: replicated compaction; P3: local relabel
-    order, label, I2, J2 = ops.compact_relabel(first, I, J, m_global, n)
-    # P4: local CSR of the shard over all n rows; global offsets = sum of the local ones
-    loc_off, loc_idx = ops.coo_to_csr(I2, J2, n)
-    offsets_g = loc_off.clone()
-    dist.all_reduce(offsets_g, op=_SUM, group=group)
-    bounds64 = row_bounds(offsets_g, m_global, P)
-    b = [int(x) for x in bounds64.cpu().tolist()]
-    cut = (loc_off.to(torch.int64) & 0xFFFFFFFF)[bounds64].cpu().tolist()     # local run ends per owner
-    send_counts = [int(cut[k + 1] - cut[k]) for k in range(P)]
-    send_t = torch.tensor(send_counts, dtype=torch.int64, device=I.device)
+    mark("first_occurrence")
+    # P2: compaction of this rank's position windows, global ranks by a prefix over the window counts
+    counts, ws = ops.compact_shard_mark(first, n, m_global, e0, ml)
+    all_counts = torch.empty(2 * P, dtype=counts.dtype, device=counts.device)
+    dist.all_gather_into_tensor(all_counts, counts, group=group)
+    label = ops.compact_shard_assign(first, n, m_global, e0, ml, all_counts, P, r, ws)
+    del ws
+    dist.all_reduce(label, op=_SUM, group=group)
+    order, hubs = ops.order_from_label(label, n)
+    mark("compact")
+    # P3: local relabel
+    I2, J2 = ops.relabel(I, J, label, hubs, n)
+    mark("relabel")
+    # P4: row cut from a coarse histogram, stable partition, all-to-all, owner's CSR
+    hist_l = ops.row_cut_hist(I2, n)
+    hist_g = hist_l.clone()
+    dist.all_reduce(hist_g, op=_SUM, group=group)
+    cut = ops.row_cut(hist_g, hist_l, n, m_global, P)
+    send_t = cut[2 * P + 2:3 * P + 2].clone()
     recv_t = torch.empty_like(send_t)
     dist.all_to_all_single(recv_t, send_t, group=group)
-    recv_counts = [int(c) for c in recv_t.cpu().tolist()]
-    lo, hi = b[r], b[r + 1]
-    rows_of = [b[k + 1] - b[k] for k in range(P)]
-    # per-row counts: owners' row ranges tile [0, n) in rank order, so the send
-    # buffer is simply the whole local count array
-    row_counts = ops.adjacent_diff(loc_off)
-    recv_rc = _alltoallv(row_counts, rows_of, [hi - lo] * P, group)
-    recv_idx = _alltoallv(loc_idx, send_counts, recv_counts, group)
-    g_lo = int((offsets_g[lo:lo + 1].to(torch.int64) & 0xFFFFFFFF).item())
-    offsets = ops.offset_ids(offsets_g[lo:hi + 1].contiguous(), -g_lo)
-    # one rank: its run is already the whole CSR
-    indices = recv_idx if P == 1 else ops.merge_rows(recv_idx, recv_rc, P, hi - lo, offsets)
-    return ShardResult(first, order, label, I2, J2, lo, hi, offsets, indices, offsets_g)
+    meta = torch.cat([cut, recv_t]).cpu().numpy().view("uint32").tolist()   # the step's one host sync
+    bounds = meta[:P + 1]
+    goff = meta[P + 1:2 * P + 2]
+    sent = meta[2 * P + 2:3 * P + 2]
+    received = meta[3 * P + 2:]
+    if P == 1:   # one owner: the shard is already the owner's edges in edge order
+        rk, rv = I2, J2
+    else:
+        keys, vals = ops.range_partition(I2, J2, cut[:P + 1], P)
+        rk = _alltoallv(keys, sent, received, group)
+        rv = _alltoallv(vals, sent, received, group)
+        del keys, vals
+    lo, hi = bounds[r], bounds[r + 1]
+    offsets, indices = ops.coo_to_csr(rk, rv, hi - lo)
+    mark("coo_to_csr")
+    return ShardResult(first, order, label, I2, J2, lo, hi, offsets, indices, goff[r], bounds, sent, received)
+
+
+def sharded_spmv(res: ShardResult, x: torch.Tensor, iters: int = 1, group=None, ops=None) -> torch.Tensor:
+    """P5: `iters` row-partitioned SpMV iterations x <- A x over the CSR that
+    sharded_reorder_to_csr left on the ranks (reference kernels.py:30-52 per
+    row range).  x (n) is replicated; after each iteration every owner
+    broadcasts its slice, so the returned vector is replicated too."""
+    ops = ops or DeviceOps()
+    P = dist.get_world_size(group)
+    b = res.bounds
+    cur = x
+    for _ in range(iters):
+        nxt = torch.empty_like(x)
+        ops.spmv(res.offsets, res.indices, cur, nxt[res.row_lo:res.row_hi])
+        works = [dist.broadcast(nxt[b[k]:b[k + 1]], src=dist.get_global_rank(group, k) if group else k,
+                                group=group, async_op=True) for k in range(P) if b[k + 1] > b[k]]
+        for w in works:
+            w.wait()
+        cur = nxt
+    return cur
 
 
 def shard_range(m_global: int, rank: int, world: int) -> tuple[int, int]:
@@ -196,3 +228,88 @@ def shard_range(m_global: int, rank: int, world: int) -> tuple[int, int]:
     base, extra = divmod(m_global, world)
     e0 = rank * base + min(rank, extra)
     return e0, e0 + base + (1 if rank < extra else 0)
+
+
+class ShardedPipeline:
+    """The sharded pipeline of one rank on fixed shard geometry, with the
+    timing hooks bench.py uses."""
+
+    PHASES = ("first_occurrence", "compact", "relabel", "coo_to_csr")
+
+    def __init__(self, n: int, m_global: int, e0: int, m_local: int, device, group=None):
+        self.n, self.m, self.e0, self.ml, self.device, self.group = n, m_global, e0, m_local, device, group
+        self.ops = DeviceOps()
+        self.last = None
+
+    def run(self, I, J, mark=None) -> ShardResult:
+        self.last = sharded_reorder_to_csr(I, J, self.n, self.m, self.e0, self.group, self.ops, mark)
+        return self.last
+
+    def phase_times(self, I, J) -> dict:
+        """One step with CUDA events at the phase boundaries; ms per phase
+        (each includes its collectives), max over ranks."""
+        evs = {}
+
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            evs[name] = e
+
+        self.run(I, J, mark)
+        torch.cuda.synchronize()
+        names = ("start",) + self.PHASES
+        t = torch.tensor([evs[a].elapsed_time(evs[b]) for a, b in zip(names, names[1:])], dtype=torch.float64,
+                         device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return {k: round(float(v), 4) for k, v in zip(self.PHASES, t.tolist())}
+
+    def spmv_timing(self, res: ShardResult, iters: int) -> dict:
+        """P5: `iters` row-partitioned SpMV iterations (x = ones), ms per
+        iteration incl. the slice broadcasts, max over ranks."""
+        x = torch.ones(self.n, dtype=torch.float32, device=self.device)
+        sharded_spmv(res, x, 1, self.group, self.ops)
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        sharded_spmv(res, x, iters, self.group, self.ops)
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        nnz = torch.tensor([res.indices.numel()], dtype=torch.float64, device=self.device)
+        dist.all_reduce(nnz, op=dist.ReduceOp.MAX, group=self.group)
+        return {"iters": iters, "x": "ones", "ms_per_iter": round(float(t.item()), 4),
+                "gedges_per_s": round(self.m / (float(t.item()) / 1e3) / 1e9, 3),
+                "max_rows_nnz_per_rank": int(nnz.item()), "balance": round(self.m / self.world / nnz.item(), 4),
+                "path": "owner rows x replicated x (boba_spmv), slices broadcast (allgather-v) per iteration"}
+
+    @property
+    def world(self) -> int:
+        return dist.get_world_size(self.group)
+
+    def comm_bytes(self) -> dict:
+        """Bytes each rank moves over NVLink per step, from the
+        last step's exchange counts, and the time they take at 900 GB/s per
+        direction."""
+        P, n = self.world, self.n
+        res = self.last
+        ring = 2 * (P - 1) / P if P > 1 else 0.0
+        sent = 8 * (sum(res.sent) - res.sent[dist.get_rank(self.group)]) if res else 0
+        b = {"allreduce_min_first": int(ring * 4 * n), "allgather_window_counts": 8 * P,
+             "allreduce_sum_label": int(ring * 4 * n),
+             "allreduce_row_hist": int(ring * 4 * int(N.lib.boba_row_cut_buckets(n))),
+             "alltoall_rows_cols_sent": int(sent)}
+        total = sum(b.values())
+        b["total"] = total
+        b["nvlink_ms_at_900gbs"] = round(total / 900e9 * 1e3, 4)
+        return b
+
+    def kernel_launches_per_step(self) -> int:
+        """Kernels one step launches (from the launch plan of each C-ABI call:
+        first occurrence 1-4 + 2 bias, window mark 3 + assign 1, order 2,
+        relabel 1-3, row-cut 2, partition 3 (+1), COO->CSR 3 per radix pass
+        + 2)."""
+        rows = max((self.last.row_hi - self.last.row_lo) if self.last else self.n // max(self.world, 1), 2)
+        passes = -(-((rows - 1).bit_length()) // 8)
+        return 4 + 2 + 4 + 2 + 2 + 2 + 3 + 3 * passes + 2

@@ -4,8 +4,10 @@ The reference package is copied (untracked) to baseline/_ref/pkg; with
 paper_2306_10410_b200.integration.patch_reference applied (via the
 ref_patch_plugin pytest plugin) its seam (_parallel first-hit / compaction /
 scatter) and its name-imported apply_permutation / coo_to_csr / spmv_pull run
-on libboba_b200.  The selected tests are exactly the ones SURVEY.md §4 lists
-as the hot path's parity suite.  Skipped when the copy is absent.
+on libboba_b200.  The selected tests are the ones SURVEY.md §4 lists as the
+hot path's parity suite, plus the reference's benchmark-record tests (its
+run_bench / compare_records drive the patched path).  The copy is made by
+tools/install_reference.sh (gitignored, shipped to the GPU box).
 """
 
 import os
@@ -30,6 +32,11 @@ SELECT = [
     "tests/test_graph.py::TestApplyPermutation",
     "tests/test_graph.py::TestDegrees",
     "tests/test_kernels.py::TestSpmv",
+    "tests/test_kernels.py::TestPageRank",
+    # the reference's own run_bench / compare_records on the patched
+    # path (checksums identical across orderings, end-to-end sums, row contract)
+    "tests/test_bench_cli.py::TestRunBench",
+    "tests/test_bench_cli.py::TestCompare",
 ]
 
 
