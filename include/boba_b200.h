@@ -163,7 +163,9 @@ int boba_reorder_to_csr_timed(const uint32_t *I, const uint32_t *J, const double
  * one eager run, which also produces outputs) into a CUDA graph; each
  * boba_graph_launch replays the whole pipeline with a single launch.  The
  * buffers must stay allocated and the input contents may change between
- * launches; (m, n) are fixed.  n >= 2. */
+ * launches; (m, n) are fixed.  n >= 2.  Creation synchronises the device
+ * first (the eager run uses a private stream, so pending writes of I and J
+ * on any caller stream must have landed). */
 typedef struct boba_graph boba_graph;
 int boba_reorder_to_csr_graph_create(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n,
                                      uint32_t *first, uint32_t *order, uint32_t *label, uint32_t *I2,

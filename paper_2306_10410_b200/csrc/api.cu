@@ -339,8 +339,12 @@ int boba_reorder_to_csr_graph_create(const uint32_t* I, const uint32_t* J, uint6
                                      uint32_t* indices, void* ws, size_t ws_bytes, boba_graph** out) {
     REQUIRE(out, "boba_reorder_to_csr_graph_create: out is NULL");
     REQUIRE(n >= 2, "boba_reorder_to_csr_graph_create: n must be >= 2 (use boba_reorder_to_csr)");
+    // the inputs may still be in flight on any of the caller's streams: the
+    // eager run below happens on a private stream, so wait for the device first
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr_graph_create: pending work");
     cudaStream_t st = nullptr;
-    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr_graph_create: stream");
     // one eager run first: one-time kernel attribute setup happens outside the capture
     int rc = boba_reorder_to_csr(I, J, nullptr, m, n, first, order, label, I2, J2, offsets, indices, nullptr, ws,
