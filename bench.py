@@ -91,7 +91,7 @@ def config_dict(cfg, world):
 def measured_traffic(cfg):
     """ncu DRAM read+write bytes per phase (profiles/traffic_<cfg>.json,
     from an ncu capture of one step of this config), or {}."""
-    for name in (f"traffic_{cfg}.json", "traffic.json" if cfg == "c2" else None):
+    for name in (f"traffic_{cfg}.json",):
         if not name:
             continue
         try:
