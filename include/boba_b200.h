@@ -312,6 +312,30 @@ int boba_row_cut_hist(const uint32_t *rows, uint64_t m_local, uint32_t n, uint32
 int boba_row_cut(const uint32_t *hist_global, const uint32_t *hist_local, uint32_t n, uint64_t m_global,
                  int world, uint32_t *out, void *stream);
 
+/* The whole sequence above in one call on the caller's NCCL communicator
+ * (nccl_comm: an ncclComm_t; libnccl.so.2 is resolved at first use,
+ * preferring the copy already loaded in the process).  Outputs: the
+ * replicated first / order / label (n words each), this rank's relabelled
+ * shard I2 / J2 (m_local), and its rows of the CSR: offsets (capacity n + 1
+ * words, local to the owned rows) and indices (capacity recv_capacity).
+ * *out gets the owned row range, the edge count and offsets[row_lo] of the
+ * global CSR; bounds_host (may be NULL, world + 1 words) every owner's rows; returns BOBA_EINVAL (with out->nnz set) if recv_capacity is
+ * too small.  One host synchronisation.  Replaces, across ranks, the
+ * reference's boba_parallel + apply_permutation + coo_to_csr
+ * (ordering.py:99-151, graph.py:253-289). */
+typedef struct boba_shard_result {
+    uint32_t row_lo, row_hi;    /* this rank owns CSR rows [row_lo, row_hi) */
+    uint64_t nnz;               /* entries of indices (edges received) */
+    uint64_t row_edge_offset;   /* global offsets[row_lo] */
+} boba_shard_result;
+size_t boba_sharded_workspace_size(uint64_t m_local, uint32_t n, int world, uint64_t recv_capacity);
+int boba_sharded_reorder_to_csr_nccl(const uint32_t *I, const uint32_t *J, uint64_t m_local, uint64_t m_global,
+                                     uint64_t e0, uint32_t n, void *nccl_comm, uint32_t *first,
+                                     uint32_t *order, uint32_t *label, uint32_t *I2, uint32_t *J2,
+                                     uint32_t *offsets, uint32_t *indices, uint64_t recv_capacity,
+                                     boba_shard_result *out, uint32_t *bounds_host, void *workspace, size_t workspace_bytes,
+                                     void *stream);
+
 /* out[i] = src[idx[i]] (permutation application on vertex arrays). */
 int boba_gather_u32(const uint32_t *src, const uint32_t *idx, uint64_t count, uint32_t *out,
                     void *stream);

@@ -76,6 +76,9 @@ SIGNATURES = {
     "boba_row_cut_buckets": ([_U32], _U32),
     "boba_row_cut_hist": ([_P, _U64, _U32, _P, _P], _I),
     "boba_row_cut": ([_P, _P, _U32, _U64, _I, _P, _P], _I),
+    "boba_sharded_workspace_size": ([_U64, _U32, _I, _U64], _SZ),
+    "boba_sharded_reorder_to_csr_nccl": ([_P, _P, _U64, _U64, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _U64, _P,
+                                          _P, _P, _SZ, _P], _I),
     "boba_reorder_to_csr_graph_create": ([_P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ,
                                           ctypes.POINTER(_P)], _I),
     "boba_graph_launch": ([_P, _P], _I),

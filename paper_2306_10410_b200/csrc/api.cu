@@ -135,6 +135,8 @@ struct boba_ctx {
 extern "C" {
 
 int boba_abi_version(void) { return 1; }
+
+int boba_sharded_fail(int code, const char* what, const char* detail) { return fail(code, "%s: %s", what, detail); }
 const char* boba_last_error(void) { return g_err.c_str(); }
 
 int boba_first_occurrence(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,

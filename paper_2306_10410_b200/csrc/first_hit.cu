@@ -54,16 +54,21 @@ __device__ __forceinline__ void update(uint32_t* first, uint32_t v, uint32_t pos
         atomicMin(first + v, pos);
 }
 
-// Dynamic mode: per-CTA set of vertices known finalised.
+// Dynamic mode: per-CTA set of vertices known finalised.  Reads happen during
+// an iteration, inserts between two barriers after it (one candidate per
+// thread, by compare-and-swap into an empty slot), so the cache is never
+// read and written concurrently; a vertex in the set is finalised, a missing
+// one only costs the guarded global check.
 template <bool RELAXED>
-__device__ __forceinline__ void hit_dyn(uint32_t* first, uint32_t* set, uint32_t v, uint32_t pos, uint32_t iter_lo) {
+__device__ __forceinline__ void hit_dyn(uint32_t* first, const uint32_t* set, uint32_t v, uint32_t pos,
+                                        uint32_t iter_lo, uint32_t& pending) {
     const uint32_t s = slot_of(v);
     if (set[s] == v) return;                       // finalised: first[v] < iter_lo <= pos
     const uint32_t cur = __ldcg(first + v);        // L2 load: may be stale (>= true value)
     if (pos < cur) {
         update<RELAXED>(first, v, pos, cur);
     } else if (cur < iter_lo && set[s] == kEmpty) {
-        set[s] = v;                                // benign race: any writer's v is finalised
+        pending = v;                               // finalised; cached after the iteration
     }
 }
 
@@ -77,7 +82,7 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* firs
     const uint64_t total_q = r.qa + r.qb;
     const uint64_t iters = ceil_div(total_q, (uint64_t)kFhNT * kFhQuads);
     for (uint64_t it = blockIdx.x; it < iters; it += gridDim.x) {
-        __syncthreads();  // every warp has left the previous iteration
+        __syncthreads();  // every warp has left the previous iteration's inserts
         const uint64_t q0 = it * kFhNT * kFhQuads;
         const uint32_t iter_lo = (uint32_t)(q0 < r.qa ? r.base_a + 4 * q0 : r.base_b + 4 * (q0 - r.qa));
         uint4 q[kFhQuads];
@@ -94,14 +99,17 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* firs
                 pos[k] = (uint32_t)(4 * qi) + (inB ? r.base_b : r.base_a);
             }
         }
+        uint32_t pending = kEmpty;
 #pragma unroll
         for (int k = 0; k < kFhQuads; k++) {
             if (!ok[k]) continue;
-            hit_dyn<RELAXED>(first, set, q[k].x, pos[k], iter_lo);
-            hit_dyn<RELAXED>(first, set, q[k].y, pos[k] + 1, iter_lo);
-            hit_dyn<RELAXED>(first, set, q[k].z, pos[k] + 2, iter_lo);
-            hit_dyn<RELAXED>(first, set, q[k].w, pos[k] + 3, iter_lo);
+            hit_dyn<RELAXED>(first, set, q[k].x, pos[k], iter_lo, pending);
+            hit_dyn<RELAXED>(first, set, q[k].y, pos[k] + 1, iter_lo, pending);
+            hit_dyn<RELAXED>(first, set, q[k].z, pos[k] + 2, iter_lo, pending);
+            hit_dyn<RELAXED>(first, set, q[k].w, pos[k] + 3, iter_lo, pending);
         }
+        __syncthreads();  // every read of this iteration is done
+        if (pending != kEmpty) atomicCAS(set + slot_of(pending), kEmpty, pending);
     }
 }
 

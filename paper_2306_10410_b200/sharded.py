@@ -40,6 +40,7 @@ gloo backend; the GPU path never imports anything but libboba_b200.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -221,6 +222,48 @@ def sharded_spmv(res: ShardResult, x: torch.Tensor, iters: int = 1, group=None, 
             w.wait()
         cur = nxt
     return cur
+
+
+class _ShardOut(ctypes.Structure):
+    _fields_ = [("row_lo", ctypes.c_uint32), ("row_hi", ctypes.c_uint32), ("nnz", ctypes.c_uint64),
+                ("row_edge_offset", ctypes.c_uint64)]
+
+
+def nccl_comm_ptr(group=None) -> int:
+    """The raw ncclComm_t of a torch.distributed NCCL process group."""
+    pg = group or dist.distributed_c10d._get_default_group()
+    return int(pg._get_backend(torch.device("cuda"))._comm_ptr())
+
+
+def native_sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: int, e0: int, group=None,
+                                  recv_capacity: int | None = None) -> ShardResult:
+    """The same pipeline as sharded_reorder_to_csr in one C-ABI call
+    (boba_sharded_reorder_to_csr_nccl) on the group's NCCL communicator: the
+    entry a C/C++ caller with its own ncclComm_t uses."""
+    P = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    dev, ml = I.device, I.numel()
+    cap = recv_capacity or (2 * m_global) // P + (1 << 20)
+    comm = ctypes.c_void_p(nccl_comm_ptr(group))
+    first, order, label = _e(n, dev), _e(n, dev), _e(n, dev)
+    I2, J2 = _e(ml, dev), _e(ml, dev)
+    offsets = _e(n + 1, dev)
+    while True:
+        indices = _e(cap, dev)
+        ws = D._ws(N.lib.boba_sharded_workspace_size(ml, n, P, cap), dev)
+        out = _ShardOut()
+        bounds = (ctypes.c_uint32 * (P + 1))()
+        rc = N.lib.boba_sharded_reorder_to_csr_nccl(
+            D._p(I), D._p(J), ml, m_global, e0, n, comm, D._p(first), D._p(order), D._p(label), D._p(I2), D._p(J2),
+            D._p(offsets), D._p(indices), cap, ctypes.byref(out), bounds, D._p(ws), ws.numel(), D._s())
+        if rc == N.BOBA_EINVAL and out.nnz > cap:
+            cap = int(out.nnz)
+            continue
+        N.check(rc)
+        break
+    lo, hi = int(out.row_lo), int(out.row_hi)
+    return ShardResult(first, order, label, I2, J2, lo, hi, offsets[:hi - lo + 1], indices[:int(out.nnz)],
+                       int(out.row_edge_offset), list(bounds), [], [])
 
 
 def shard_range(m_global: int, rank: int, world: int) -> tuple[int, int]:

@@ -149,6 +149,17 @@ def test_sharded_pipeline_one_rank_nccl(ops):
         x = np.random.default_rng(1).random(n, dtype=np.float32)
         y = sharded_spmv(res, torch.from_numpy(x).cuda(), 1).cpu().numpy()
         np.testing.assert_allclose(y, oracle.spmv_pull(off, idx, x.astype(np.float64)), rtol=1e-5, atol=0)
+        # the same pipeline through the one-call C-ABI entry on torch's NCCL communicator
+        from paper_2306_10410_b200.sharded import native_sharded_reorder_to_csr
+
+        nat = native_sharded_reorder_to_csr(cu(I), cu(J), n, I.size, 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(nat.order), order) and np.array_equal(host(nat.label), label)
+        assert np.array_equal(host(nat.I2), I2) and np.array_equal(host(nat.J2), J2)
+        assert (nat.row_lo, nat.row_hi, nat.row_edge_offset) == (0, n, 0) and nat.bounds == [0, n]
+        assert np.array_equal(host(nat.offsets), off) and np.array_equal(host(nat.indices), idx)
+        small = native_sharded_reorder_to_csr(cu(I), cu(J), n, I.size, 0, recv_capacity=100)   # grows and retries
+        assert np.array_equal(host(small.indices), idx)
         ph = sp.phase_times(cu(I), cu(J))
         assert set(ph) == set(sp.PHASES) and all(v > 0 for v in ph.values())
         assert sp.spmv_timing(res, 2)["ms_per_iter"] > 0
