@@ -318,10 +318,13 @@ int boba_reorder_to_csr_timed(const uint32_t* I, const uint32_t* J, const double
     e = boba::launch_compact(first, m, n, order, label, nullptr, hubs, rest, rest_bytes, sms, s);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: compact");
     mark(2);
-    e = boba::launch_relabel(I, J, m, label, hubs, I2, J2, nullptr, n, sms, s);
+    // the relabel may also count the first radix digit of its rows (the
+    // COO->CSR workspace `rest` is idle until then)
+    boba::RowTileHist rh = boba::coo_to_csr_first_hist(rest, rest_bytes, m, n, w != nullptr);
+    e = boba::launch_relabel(I, J, m, label, hubs, I2, J2, nullptr, n, sms, s, &rh);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: relabel");
     mark(3);
-    e = boba::launch_coo_to_csr(I2, J2, w, m, n, nullptr, offsets, indices, w_out, rest, rest_bytes, sms, s);
+    e = boba::launch_coo_to_csr(I2, J2, w, m, n, nullptr, offsets, indices, w_out, rest, rest_bytes, sms, s, rh.done);
     (void)counts;
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: coo_to_csr");
     mark(4);

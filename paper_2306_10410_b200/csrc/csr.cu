@@ -272,7 +272,7 @@ CsrWs carve(void* base, uint64_t m, uint32_t n) {
 template <int RB, int NT, int IPT, int MINB, typename Op = DigitShift>
 cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, Op op, int bits, uint32_t* H,
                           unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                          int num_sms, cudaStream_t s, uint32_t* row_starts = nullptr) {
+                          int num_sms, cudaStream_t s, uint32_t* row_starts = nullptr, bool h_ready = false) {
     using C = RadixCfg<RB, NT, IPT>;
     static PerDeviceOnce attr;
     if (cudaError_t e = set_attr_once(attr, k_radix_downsweep<RB, NT, IPT, MINB, Op>,
@@ -281,7 +281,7 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
     const uint64_t tiles = ceil_div(m, C::TILE);
     const uint64_t hcount = tiles << bits;
     const uint64_t up_grid = tiles < (uint64_t)num_sms * 8 ? tiles : (uint64_t)num_sms * 8;
-    k_radix_upsweep<RB, NT, IPT, Op><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, op, bits, tiles, H);
+    if (!h_ready) k_radix_upsweep<RB, NT, IPT, Op><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, op, bits, tiles, H);
     cudaError_t e = cudaMemsetAsync(scan_status, 0, (ceil_div(hcount, kScanTile) + 1) * 8, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 4, s);
     if (e != cudaSuccess) return e;
@@ -296,21 +296,32 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
 template <int RB, int NT, int IPT, int MINB>
 cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits, uint32_t* H,
                        unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                       int num_sms, cudaStream_t s, uint32_t* row_starts) {
+                       int num_sms, cudaStream_t s, uint32_t* row_starts, bool h_ready = false) {
     const DigitShift op{shift, (1u << bits) - 1u};
     if (RB == 8 && bits <= 6)
         return radix_pass_op<6, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                           num_sms, s, row_starts);
+                                                           num_sms, s, row_starts, h_ready);
     if (RB == 8 && bits == 7)
         return radix_pass_op<7, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                           num_sms, s, row_starts);
+                                                           num_sms, s, row_starts, h_ready);
     return radix_pass_op<RB, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                        num_sms, s, row_starts);
+                                                        num_sms, s, row_starts, h_ready);
 }
 
 }  // namespace
 
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool /*weighted*/) { return carve(nullptr, m, n).total; }
+
+RowTileHist coo_to_csr_first_hist(void* ws, size_t ws_bytes, uint64_t m, uint32_t n, bool /*weighted*/) {
+    RowTileHist r;
+    const CsrPlan p = plan_for(n);
+    const CsrWs W = carve(ws, m, n);
+    if (!ws || ws_bytes < W.total || p.passes == 0 || m == 0 || p.tile != 4096) return r;
+    r.H = W.H;
+    r.tiles = ceil_div(m, p.tile);
+    r.mask = (1u << p.bits[0]) - 1u;
+    return r;
+}
 
 
 __global__ void k_iota(uint32_t* out, uint64_t count) {
@@ -455,7 +466,7 @@ cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* cou
 
 cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
                               const uint32_t* counts_in, uint32_t* offsets, uint32_t* indices, double* w_out,
-                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s) {
+                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool first_hist_ready) {
     const bool weighted = w != nullptr;
     CsrWs W = carve(ws, m, n);
     if (ws_bytes < W.total) return cudaErrorInvalidValue;
@@ -493,7 +504,7 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
         uint32_t* kout = last ? nullptr : W.bufs[(i & 1) * 2];
         uint32_t* vout = (last && !weighted) ? indices : W.bufs[(i & 1) * 2 + 1];
         e = radix_pass<8, 256, 16, 4>(kin, vin, m, p.shift[i], p.bits[i], W.H, W.scan_status, W.counters, kout, vout,
-                                      num_sms, s, (last && !counts_in) ? offsets : nullptr);
+                                      num_sms, s, (last && !counts_in) ? offsets : nullptr, i == 0 && first_hist_ready);
         if (e != cudaSuccess) return e;
         kin = kout;
         vin = vout;

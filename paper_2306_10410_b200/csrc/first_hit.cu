@@ -27,6 +27,8 @@
 #include "hubs.cuh"
 #include "kernels.cuh"
 
+#include <type_traits>
+
 namespace boba {
 
 constexpr int kFhNT = 1024;              // threads per CTA (one CTA per SM)
@@ -45,6 +47,7 @@ struct Ranges {
 };
 
 __device__ __forceinline__ uint32_t slot_of(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - kFhSlotsLog2); }
+__device__ __forceinline__ uint32_t hash_slot(uint32_t v) { return (v * 0x85EBCA6Bu) ^ (v >> 13); }
 
 template <bool RELAXED>
 __device__ __forceinline__ void update(uint32_t* first, uint32_t v, uint32_t pos, uint32_t cur) {
@@ -117,18 +120,23 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* firs
 // separately (uniform pointer and base, no per-quad range select), SeenSet
 // membership is a SWAR zero-lane test on the bucket's 64 bits, and the guard
 // load and the atomicMin are predicated instructions, not branches.
+// SeenSet membership: a SWAR zero-lane test on each of the bucket's three
+// 32-bit words (planes: word w of bucket b at set[w * kHubBuckets + b]).
 template <int TW>
-__device__ __forceinline__ bool seen_swar(const unsigned long long* set, const HubHash& hh, uint32_t v) {
+__device__ __forceinline__ bool seen_swar(const uint32_t* set, const HubHash& hh, uint32_t v) {
     constexpr uint32_t kTagMask = (1u << TW) - 1u;
     constexpr uint32_t kOnes = TW == 8 ? 0x01010101u : 0x00010001u;
     constexpr uint32_t kHigh = kOnes << (TW - 1);
     uint32_t b, tag;
     hh.split(v, b, tag);
-    const uint2 w = reinterpret_cast<const uint2*>(set)[b];
     const uint32_t rep = tag * kOnes;
-    const uint32_t x0 = w.x ^ rep, x1 = w.y ^ rep;  // a lane equal to tag -> a zero lane
-    const uint32_t z = (((x0 - kOnes) & ~x0) | ((x1 - kOnes) & ~x1)) & kHigh;
-    return z != 0 && tag != kTagMask;               // all-ones tags are never inserted (empty marker)
+    uint32_t z = 0;
+#pragma unroll
+    for (int w = 0; w < kSeenPlanes; w++) {
+        const uint32_t x = set[w * kHubBuckets + b] ^ rep;  // a lane equal to tag -> a zero lane
+        z |= (x - kOnes) & ~x;
+    }
+    return (z & kHigh) != 0 && tag != kTagMask;        // all-ones tags are never inserted (empty marker)
 }
 
 __device__ __forceinline__ uint32_t ld_cg_pred(const uint32_t* p, bool pred) {
@@ -158,7 +166,7 @@ __device__ __forceinline__ void red_min_pred(uint32_t* p, uint32_t v, bool pred)
 // flight).
 template <int TW, bool BITS>
 __device__ __forceinline__ void sweep_static(const uint4* __restrict__ src, uint64_t nq, uint32_t base,
-                                             uint32_t* first, const unsigned long long* set, const HubHash& hh,
+                                             uint32_t* first, const uint32_t* set, const HubHash& hh,
                                              const uint32_t* __restrict__ seenb, uint32_t* newb) {
     constexpr uint64_t kIter = (uint64_t)kFhNT * kFhQuads;
     const uint64_t iters = ceil_div(nq, kIter);
@@ -207,19 +215,21 @@ __device__ __forceinline__ void sweep_static(const uint4* __restrict__ src, uint
 
 template <int TW, bool BITS>
 __global__ void __launch_bounds__(kFhNT, 1) k_first_hit_static(Ranges r, uint32_t* first,
-                                                               const unsigned long long* __restrict__ seen_g,
+                                                               const uint32_t* __restrict__ seen_g,
                                                                HubHash hh, const uint32_t* seenb, uint32_t* newb) {
-    extern __shared__ unsigned long long smem_u64[];
-    for (int i = threadIdx.x; i < kHubBuckets; i += kFhNT) smem_u64[i] = __ldg(seen_g + i);
+    extern __shared__ uint4 smem_u128[];
+    uint32_t* set = reinterpret_cast<uint32_t*>(smem_u128);
+    for (int i = threadIdx.x; i < (int)(kSeenSetBytes / 16); i += kFhNT)
+        smem_u128[i] = __ldg(reinterpret_cast<const uint4*>(seen_g) + i);
     __syncthreads();
-    sweep_static<TW, BITS>(reinterpret_cast<const uint4*>(r.a), r.qa, r.base_a, first, smem_u64, hh, seenb, newb);
-    sweep_static<TW, BITS>(reinterpret_cast<const uint4*>(r.b), r.qb, r.base_b, first, smem_u64, hh, seenb, newb);
+    sweep_static<TW, BITS>(reinterpret_cast<const uint4*>(r.a), r.qa, r.base_a, first, set, hh, seenb, newb);
+    sweep_static<TW, BITS>(reinterpret_cast<const uint4*>(r.b), r.qb, r.base_b, first, set, hh, seenb, newb);
 }
 
 template <int TW, bool BITS = false>
-static void launch_static(const Ranges& r, uint32_t* first, const unsigned long long* seen_g, const HubHash& hh,
+static void launch_static(const Ranges& r, uint32_t* first, const uint32_t* seen_g, const HubHash& hh,
                           int num_sms, cudaStream_t s, const uint32_t* seenb = nullptr, uint32_t* newb = nullptr) {
-    const size_t smem = sizeof(unsigned long long) * kHubBuckets;
+    const size_t smem = kSeenSetBytes;
     static PerDeviceOnce attr;
     set_attr_once(attr, k_first_hit_static<TW, BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_first_hit_static<TW, BITS><<<num_sms, kFhNT, smem, s>>>(r, first, seen_g, hh, seenb, newb);
@@ -237,30 +247,46 @@ __global__ void k_merge_bits(uint32_t* seenb, uint32_t* newb, uint64_t words) {
     }
 }
 
-// SeenSet from the prefix: every vertex whose first occurrence is one of the
-// prefix positions gets its tag into a free 16-bit lane of its bucket.
+// SeenSet from the counting prefix: a vertex whose first occurrence is one of
+// the prefix positions (exactly one thread per vertex) and whose prefix count
+// reaches `thr` gets its tag into a free lane of its bucket.  Two rounds
+// (frequent vertices first, then any) fill the lanes in priority order; a
+// full bucket drops the vertex: membership only ever saves work, it never
+// changes first[].  Without counts (cnt == NULL) every such vertex is offered.
 template <int TW>
 __global__ void k_seen_build(const uint32_t* __restrict__ I, uint32_t count, uint32_t base,
-                             const uint32_t* __restrict__ first, HubHash hh, unsigned long long* set) {
-    constexpr unsigned long long kTagMask = (1ull << TW) - 1ull;
+                             const uint32_t* __restrict__ first, HubHash hh, const uint32_t* __restrict__ cnt,
+                             uint32_t cmask, uint32_t thr, uint32_t* set) {
+    constexpr uint32_t kTagMask = (1u << TW) - 1u;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= count) return;
     const uint32_t v = __ldg(I + p);
-    if (__ldg(first + v) != base + p) return;   // not the first occurrence (exactly one thread per vertex)
+    if (__ldg(first + v) != base + p) return;   // not the first occurrence
+    if (cnt && __ldg(cnt + (hash_slot(v) & cmask)) < thr) return;
     uint32_t b, tag;
     hh.split(v, b, tag);
     if (tag == kTagMask) return;                // reserved for "empty"
-    unsigned long long w = set[b];
-    while (true) {
-        int lane = -1;
-        for (int l = 0; l < 64 / TW; l++)
-            if (((w >> (TW * l)) & kTagMask) == kTagMask) { lane = l; break; }
-        if (lane < 0) return;                   // bucket full: not recorded (still correct)
-        const unsigned long long nw = (w & ~(kTagMask << (TW * lane))) | ((unsigned long long)tag << (TW * lane));
-        const unsigned long long old = atomicCAS(set + b, w, nw);
-        if (old == w) return;
-        w = old;
+    for (int pl = 0; pl < kSeenPlanes; pl++) {
+        uint32_t* wp = set + pl * kHubBuckets + b;
+        uint32_t w = *wp;
+        while (true) {
+            int lane = -1;
+            for (int l = 0; l < 32 / TW; l++)
+                if (((w >> (TW * l)) & kTagMask) == kTagMask) { lane = l; break; }
+            if (lane < 0) break;                // word full: next plane
+            const uint32_t nw = (w & ~(kTagMask << (TW * lane))) | (tag << (TW * lane));
+            const uint32_t old = atomicCAS(wp, w, nw);
+            if (old == w) return;
+            w = old;
+        }
     }
+}
+
+// Frequency of every vertex in the counting prefix (hashed slots: a collision
+// only merges two counts, which can only change the set's choice).
+__global__ void k_prefix_count(const uint32_t* __restrict__ I, uint32_t count, uint32_t cmask, uint32_t* cnt) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < count) atomicAdd(cnt + (hash_slot(__ldg(I + p)) & cmask), 1u);
 }
 
 // Stage 1 of the two-stage sweep: guarded atomicMin over the prefix of I, one
@@ -313,13 +339,21 @@ size_t first_hit_workspace_bytes() { return kHubTableBytes; }
 // A contiguous shard [e0, e0 + m) of a global edge list with m_global edges:
 // local I[i] sits at global position e0 + i, local J[i] at m_global + e0 + i.
 // `seen_ws` (kHubTableBytes, may be NULL) enables the two-stage sweep.
-size_t first_hit_bits_workspace_bytes(uint32_t n) { return 2 * (((uint64_t)n + 31) / 32 * 4 + 256); }
+// The prefix count table (kCountSlots words + the 256-bin histogram and the
+// threshold) shares it: it is dead before the waves clear their bitmaps.
+constexpr uint32_t kCountSlots = 1u << 21;
+constexpr size_t kCountBytes = (size_t)kCountSlots * 4;
+constexpr uint32_t kSeenHot = 4;  // first round: vertices seen at least this often in the prefix
+size_t first_hit_bits_workspace_bytes(uint32_t n) {
+    const size_t bits = 2 * (((uint64_t)n + 31) / 32 * 4 + 256);
+    return bits > kCountBytes ? bits : kCountBytes;
+}
 
 // Static sweep of r in waves of kFhWave positions (BITS mode, see sweep_static).
 constexpr uint64_t kFhWaveQuads = (1ull << 26) / 4;
 
 template <int TW>
-static cudaError_t launch_static_waves(const Ranges& r, uint32_t* first, const unsigned long long* set,
+static cudaError_t launch_static_waves(const Ranges& r, uint32_t* first, const uint32_t* set,
                                        const HubHash& hh, uint32_t n, void* bits_ws, int num_sms, cudaStream_t s) {
     const uint64_t words = ((uint64_t)n + 31) / 32;
     uint32_t* seenb = static_cast<uint32_t*>(bits_ws);
@@ -357,26 +391,42 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
     uint64_t done = 0;
     if (vec && m >= 4) {
         const uint64_t quads = m >> 2;
-        const uint32_t prefix = seen_prefix(hh.tag_bits);
+        // counting prefix: the largest power of two <= min(seen_prefix, m / 256), at least 64K
+        uint32_t prefix = seen_prefix(hh.tag_bits);
+        while (prefix > 65536u && 256ull * prefix > m) prefix >>= 1;
         const bool two_stage = seen_ws && !relaxed && hh.tag_bits <= 16 && m >= 16ull * prefix;
         if (two_stage) {
-            unsigned long long* set = static_cast<unsigned long long*>(seen_ws);
+            uint32_t* set = static_cast<uint32_t*>(seen_ws);
             const uint64_t qp = prefix / 4;
             // stage 1 fully parallel (the ordered persistent sweep ran on only a few CTAs
             // for a 128K-position prefix: 20 us vs 8 us)
             k_first_hit_prefix<<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first);
-            err = cudaMemsetAsync(set, 0xFF, kHubTableBytes, s);
+            err = cudaMemsetAsync(set, 0xFF, kSeenSetBytes, s);
             if (err != cudaSuccess) return err;
+            // the set's members: the prefix's first-seen vertices, most frequent first
+            uint32_t* cnt = bits_ws ? static_cast<uint32_t*>(bits_ws) : nullptr;
+            const uint32_t cmask = kCountSlots - 1;
+            const unsigned pg = (unsigned)ceil_div(prefix, 256);
+            if (cnt) {
+                err = cudaMemsetAsync(cnt, 0, kCountBytes, s);
+                if (err != cudaSuccess) return err;
+                k_prefix_count<<<pg, 256, 0, s>>>(I, prefix, cmask, cnt);
+            }
+            auto build = [&](auto tw) {
+                constexpr int TW = decltype(tw)::value;
+                if (cnt) k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, kSeenHot, set);
+                k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, 1u, set);
+            };
             Ranges r2{I + prefix, quads - qp, base_i + prefix, J, quads, base_j};
             // first[] beyond L2 (n > 2^24, > 64 MB): guard on a seen-bitmap in waves instead of
             // first[] itself (measured: s26 18.0 -> 9.3 ms; s24, table still partly in L2: 1.90 vs 2.35)
             const bool waves = bits_ws && n > (1u << 24);
             if (hh.tag_bits <= 8) {
-                k_seen_build<8><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
+                build(std::integral_constant<int, 8>{});
                 if (waves) err = launch_static_waves<8>(r2, first, set, hh, n, bits_ws, num_sms, s);
                 else launch_static<8>(r2, first, set, hh, num_sms, s);
             } else {
-                k_seen_build<16><<<(unsigned)ceil_div(prefix, 256), 256, 0, s>>>(I, prefix, base_i, first, hh, set);
+                build(std::integral_constant<int, 16>{});
                 if (waves) err = launch_static_waves<16>(r2, first, set, hh, n, bits_ws, num_sms, s);
                 else launch_static<16>(r2, first, set, hh, num_sms, s);
             }

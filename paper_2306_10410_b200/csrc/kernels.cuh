@@ -25,18 +25,31 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
                            uint32_t* n_seen_out, unsigned long long* hubs, void* ws, size_t ws_bytes, int num_sms,
                            cudaStream_t s);
 
+// The first radix pass of COO->CSR needs the digit histogram of every
+// 4096-row tile of I2; the relabel that writes I2 can produce it on the way
+// (csr.cu decides where it lives and which digit; H == NULL: not wanted).
+struct RowTileHist {
+    uint32_t* H = nullptr;  // digit-major: H[d * tiles + t]
+    uint64_t tiles = 0;
+    uint32_t mask = 0;      // digit = row & mask (the first pass has shift 0)
+    bool done = false;      // set by launch_relabel when it wrote H
+};
+RowTileHist coo_to_csr_first_hist(void* ws, size_t ws_bytes, uint64_t m, uint32_t n, bool weighted);
+
 // counts (may be NULL): also the out-degree histogram of the new rows
 cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,
                            const unsigned long long* hubs, uint32_t* I2, uint32_t* J2, uint32_t* counts, uint32_t n,
-                           int num_sms, cudaStream_t s);
+                           int num_sms, cudaStream_t s, RowTileHist* row_hist = nullptr);
 
 cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* counts, int num_sms, cudaStream_t s);
 cudaError_t launch_row_offsets(const uint32_t* counts, uint32_t n, uint32_t* offsets, unsigned long long* status,
                                unsigned* counter, cudaStream_t s);
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool weighted);
+// first_hist_ready: the relabel already wrote the first pass's tile histogram
+// (coo_to_csr_first_hist of the same workspace)
 cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
                               const uint32_t* counts_in, uint32_t* offsets, uint32_t* indices, double* w_out,
-                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s);
+                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool first_hist_ready = false);
 
 size_t spmv_workspace_bytes(uint32_t n, uint64_t m);
 cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,

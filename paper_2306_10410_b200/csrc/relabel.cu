@@ -120,10 +120,28 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel(const uint4* __restrict__ 
 // their range (n <= 2^31, so the flag bit is free).
 constexpr uint32_t kRlFlag = 0x80000000u;
 
-template <bool FIRST>
+// HIST (last pass only, when every id is final): the CTA's iteration t covers
+// edges [4096 t, 4096 t + 4096) -- exactly radix tile t of COO->CSR -- so it
+// also counts the first radix digit of its I2 rows in shared memory and
+// writes the tile's column of H; the COO->CSR skips its first upsweep.  Two
+// alternating histograms: each is flushed and cleared while the next
+// iteration counts into the other, one barrier per iteration.
+constexpr int kRlHistMax = 256;
+static_assert(kRlNT * 4 == 4096, "relabel iteration = radix tile");
+
+template <bool FIRST, bool HIST>
 __global__ void __launch_bounds__(kRlNT, 1) k_relabel_range(const uint4* __restrict__ I, const uint4* __restrict__ J,
                                                             uint64_t quads, const uint32_t* __restrict__ label,
-                                                            uint32_t lo, uint32_t width, uint4* I2, uint4* J2) {
+                                                            uint32_t lo, uint32_t width, uint4* I2, uint4* J2,
+                                                            RowTileHist rh) {
+    // HIST: TPI tiles per iteration, so the barrier comes once per 16K edges
+    constexpr int TPI = HIST ? 4 : 1;
+    __shared__ uint32_t s_h[2][TPI][HIST ? kRlHistMax : 1];
+    if (HIST) {
+        for (int i = threadIdx.x; i < 2 * TPI * kRlHistMax; i += kRlNT) (&s_h[0][0][0])[i] = 0;
+        __syncthreads();
+    }
+    int par = 0;
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     auto fix = [&](uint32_t v) -> uint32_t {
@@ -132,15 +150,43 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel_range(const uint4* __restr
         if (id - lo < width) return ld_label(label + id, true, pol);
         return id | kRlFlag;
     };
-    for (uint64_t t = blockIdx.x; t * kRlNT < quads; t += gridDim.x) {
-        const uint64_t q = t * kRlNT + threadIdx.x;
-        if (q < quads) {
-            const uint4 a = FIRST ? __ldcs(I + q) : __ldcs(I2 + q), b = FIRST ? __ldcs(J + q) : __ldcs(J2 + q);
-            uint4 ra, rb;
-            ra.x = fix(a.x); ra.y = fix(a.y); ra.z = fix(a.z); ra.w = fix(a.w);
-            rb.x = fix(b.x); rb.y = fix(b.y); rb.z = fix(b.z); rb.w = fix(b.w);
-            __stcs(I2 + q, ra);
-            __stcs(J2 + q, rb);
+    for (uint64_t g = blockIdx.x; g * TPI * kRlNT < quads; g += gridDim.x) {
+        uint4 a[TPI], b[TPI];
+#pragma unroll
+        for (int k = 0; k < TPI; k++) {
+            const uint64_t q = (g * TPI + k) * kRlNT + threadIdx.x;
+            if (q < quads) {
+                a[k] = FIRST ? __ldcs(I + q) : __ldcs(I2 + q);
+                b[k] = FIRST ? __ldcs(J + q) : __ldcs(J2 + q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < TPI; k++) {
+            const uint64_t q = (g * TPI + k) * kRlNT + threadIdx.x;
+            if (q < quads) {
+                uint4 ra, rb;
+                ra.x = fix(a[k].x); ra.y = fix(a[k].y); ra.z = fix(a[k].z); ra.w = fix(a[k].w);
+                rb.x = fix(b[k].x); rb.y = fix(b[k].y); rb.z = fix(b[k].z); rb.w = fix(b[k].w);
+                __stcs(I2 + q, ra);
+                __stcs(J2 + q, rb);
+                if (HIST) {
+                    uint32_t* h = s_h[par][k];
+                    atomicAdd(h + (ra.x & rh.mask), 1u);
+                    atomicAdd(h + (ra.y & rh.mask), 1u);
+                    atomicAdd(h + (ra.z & rh.mask), 1u);
+                    atomicAdd(h + (ra.w & rh.mask), 1u);
+                }
+            }
+        }
+        if (HIST) {
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < (uint32_t)TPI * (rh.mask + 1); i += kRlNT) {
+                const uint32_t k = i / (rh.mask + 1), d = i % (rh.mask + 1);
+                const uint64_t t = g * TPI + k;
+                if (t < rh.tiles) rh.H[(uint64_t)d * rh.tiles + t] = s_h[par][k][d];
+                s_h[par][k][d] = 0;
+            }
+            par ^= 1;
         }
     }
 }
@@ -170,7 +216,8 @@ static void launch_vec(int grid, size_t smem, cudaStream_t s, const uint32_t* I,
 
 cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,
                            const unsigned long long* hubs, uint32_t* I2, uint32_t* J2, uint32_t* counts, uint32_t n,
-                           int num_sms, cudaStream_t s) {
+                           int num_sms, cudaStream_t s, RowTileHist* row_hist) {
+    if (row_hist) row_hist->done = false;
     if (counts) {
         cudaError_t err = cudaMemsetAsync(counts, 0, (size_t)n * 4, s);
         if (err != cudaSuccess) return err;
@@ -204,15 +251,28 @@ cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, con
                 launch_vec<0, false, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
             } else {
                 const uint32_t width = (uint32_t)ceil_div(n, passes);
+                // the last pass also counts the first radix digit per tile (no scalar tail:
+                // every edge is in a quad, so the tiles are complete)
+                const bool hist = row_hist && row_hist->H && (m & 3) == 0 && row_hist->mask < kRlHistMax &&
+                                  row_hist->tiles == ceil_div(m, 4096);
+                const RowTileHist rh = hist ? *row_hist : RowTileHist{};
                 for (uint32_t p = 0; p < passes; p++) {
                     const uint32_t lo = p * width;
+                    const bool last = p + 1 == passes;
                     if (p == 0)
-                        k_relabel_range<true><<<grid, kRlNT, 0, s>>>((const uint4*)I, (const uint4*)J, quads, label,
-                                                                     lo, width, (uint4*)I2, (uint4*)J2);
+                        k_relabel_range<true, false><<<grid, kRlNT, 0, s>>>((const uint4*)I, (const uint4*)J, quads,
+                                                                            label, lo, width, (uint4*)I2, (uint4*)J2,
+                                                                            rh);
+                    else if (last && hist)
+                        k_relabel_range<false, true><<<grid, kRlNT, 0, s>>>((const uint4*)I2, (const uint4*)J2, quads,
+                                                                            label, lo, width, (uint4*)I2, (uint4*)J2,
+                                                                            rh);
                     else
-                        k_relabel_range<false><<<grid, kRlNT, 0, s>>>((const uint4*)I2, (const uint4*)J2, quads,
-                                                                      label, lo, width, (uint4*)I2, (uint4*)J2);
+                        k_relabel_range<false, false><<<grid, kRlNT, 0, s>>>((const uint4*)I2, (const uint4*)J2,
+                                                                             quads, label, lo, width, (uint4*)I2,
+                                                                             (uint4*)J2, rh);
                 }
+                if (hist) row_hist->done = true;
             }
         } else {
             if (hubs) launch_vec<0, true>(grid, smem, s, I, J, quads, label, hubs, n, I2, J2, counts);
