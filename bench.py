@@ -787,6 +787,8 @@ def run_sharded(args):
     phases = sp.phase_times(I, J)  # one more step with events at the phase boundaries
     # row-partitioned SpMV (P5): x replicated, y slices allgathered between iterations
     spmv = sp.spmv_timing(res, SPMV_ITERS[cfg])
+    # the same iterations with each owner's slice broadcast piece by piece while it computes the next
+    spmv["overlapped"] = sp.spmv_timing(res, SPMV_ITERS[cfg], chunks=4)
 
     # end to end: pinned host shard -> device, sharded pipeline, local CSR back to pinned host buffers
     hI = torch.empty(e1 - e0, dtype=torch.int32, pin_memory=True)

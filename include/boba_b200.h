@@ -66,8 +66,9 @@ int boba_first_occurrence(const uint32_t *I, const uint32_t *J, uint64_t m, uint
  * chunk-local-min merge, _parallel.py:139-162.
  * workspace (may be NULL; boba_first_occurrence_workspace_size() bytes)
  * enables the two-stage sweep with the shared-memory SeenSet of hubs; with
- * boba_first_occurrence_shard_workspace_size(n) bytes, also the wave-guarded
- * sweep the fused single-GPU call uses beyond L2 (n > 2^24). */
+ * boba_first_occurrence_shard_workspace_size(n) bytes, also the prefix count
+ * table that fills the SeenSet with the most frequent vertices first, and the
+ * wave-guarded sweep the fused single-GPU call uses beyond L2 (n > 2^24). */
 size_t boba_first_occurrence_workspace_size(void);
 size_t boba_first_occurrence_shard_workspace_size(uint32_t n);
 int boba_first_occurrence_shard(const uint32_t *I, const uint32_t *J, uint64_t m_local,

@@ -153,7 +153,8 @@ def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int
 def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: int, e0: int, group=None,
                            ops=None, mark=None) -> ShardResult:
     """Run the BOBA pipeline on this rank's contiguous shard (see module doc).
-    `mark(name)`, if given, is called at every phase boundary (timing)."""
+    `mark(name)`, if given, is called at every phase boundary (timing) and
+    with "+comm" / "-comm" around every collective."""
     ops = ops or DeviceOps()
     mark = mark or (lambda name: None)
     P = dist.get_world_size(group)
@@ -163,16 +164,22 @@ def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: i
     # P1: local first occurrence, exact global merge
     first = ops.first_occurrence_shard(I, J, m_global, e0, n)
     key = ops.bias(first)
+    mark("+comm")
     dist.all_reduce(key, op=_MIN, group=group)
+    mark("-comm")
     first = ops.bias(key)
     mark("first_occurrence")
     # P2: compaction of this rank's position windows, global ranks by a prefix over the window counts
     counts, ws = ops.compact_shard_mark(first, n, m_global, e0, ml)
     all_counts = torch.empty(2 * P, dtype=counts.dtype, device=counts.device)
+    mark("+comm")
     dist.all_gather_into_tensor(all_counts, counts, group=group)
+    mark("-comm")
     label = ops.compact_shard_assign(first, n, m_global, e0, ml, all_counts, P, r, ws)
     del ws
+    mark("+comm")
     dist.all_reduce(label, op=_SUM, group=group)
+    mark("-comm")
     order, hubs = ops.order_from_label(label, n)
     mark("compact")
     # P3: local relabel
@@ -181,11 +188,15 @@ def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: i
     # P4: row cut from a coarse histogram, stable partition, all-to-all, owner's CSR
     hist_l = ops.row_cut_hist(I2, n)
     hist_g = hist_l.clone()
+    mark("+comm")
     dist.all_reduce(hist_g, op=_SUM, group=group)
+    mark("-comm")
     cut = ops.row_cut(hist_g, hist_l, n, m_global, P)
     send_t = cut[2 * P + 2:3 * P + 2].clone()
     recv_t = torch.empty_like(send_t)
+    mark("+comm")
     dist.all_to_all_single(recv_t, send_t, group=group)
+    mark("-comm")
     meta = torch.cat([cut, recv_t]).cpu().numpy().view("uint32").tolist()   # the step's one host sync
     bounds = meta[:P + 1]
     goff = meta[P + 1:2 * P + 2]
@@ -195,8 +206,10 @@ def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: i
         rk, rv = I2, J2
     else:
         keys, vals = ops.range_partition(I2, J2, cut[:P + 1], P)
+        mark("+comm")
         rk = _alltoallv(keys, sent, received, group)
         rv = _alltoallv(vals, sent, received, group)
+        mark("-comm")
         del keys, vals
     lo, hi = bounds[r], bounds[r + 1]
     offsets, indices = ops.coo_to_csr(rk, rv, hi - lo)
@@ -204,20 +217,73 @@ def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: i
     return ShardResult(first, order, label, I2, J2, lo, hi, offsets, indices, goff[r], bounds, sent, received)
 
 
-def sharded_spmv(res: ShardResult, x: torch.Tensor, iters: int = 1, group=None, ops=None) -> torch.Tensor:
+def _chunk_rows(b0: int, b1: int, c: int, chunks: int) -> tuple[int, int]:
+    """Row range [r0, r1) of chunk c of an owner's rows [b0, b1): equal row
+    counts, so every rank knows every owner's chunks from the bounds alone."""
+    k = b1 - b0
+    return b0 + c * k // chunks, b0 + (c + 1) * k // chunks
+
+
+def _spmv_pieces(res: ShardResult, chunks: int) -> list:
+    """The owner's CSR cut into `chunks` row pieces (offsets re-based to their
+    first nonzero), built once per (result, chunks)."""
+    cache = res.__dict__.setdefault("_spmv_pieces", {})
+    if chunks not in cache:
+        pieces = []
+        off = res.offsets
+        for c in range(chunks):
+            r0, r1 = _chunk_rows(0, res.row_hi - res.row_lo, c, chunks)
+            if r1 == r0:
+                pieces.append(None)
+                continue
+            o = off[r0:r1 + 1]
+            base = o[:1]
+            lo_hi = torch.stack([o[0], o[-1]]).to(torch.int64).cpu().tolist()   # setup-time host read
+            pieces.append((r0, r1, o - base, res.indices[lo_hi[0] & 0xFFFFFFFF:lo_hi[1] & 0xFFFFFFFF]))
+        cache[chunks] = pieces
+    return cache[chunks]
+
+
+def sharded_spmv(res: ShardResult, x: torch.Tensor, iters: int = 1, group=None, ops=None,
+                 chunks: int = 1) -> torch.Tensor:
     """P5: `iters` row-partitioned SpMV iterations x <- A x over the CSR that
     sharded_reorder_to_csr left on the ranks (reference kernels.py:30-52 per
     row range).  x (n) is replicated; after each iteration every owner
-    broadcasts its slice, so the returned vector is replicated too."""
+    broadcasts its slice, so the returned vector is replicated too.
+
+    chunks > 1 overlaps the exchange with the multiply: each
+    owner's rows are cut into `chunks` equal row pieces; piece c of every
+    owner is broadcast (asynchronously, on the collective's own stream) as
+    soon as its owner has computed it, while the owner computes piece c + 1.
+    Every rank issues the broadcasts in the same (piece, owner) order."""
     ops = ops or DeviceOps()
     P = dist.get_world_size(group)
     b = res.bounds
+    src = [dist.get_global_rank(group, k) if group else k for k in range(P)]
     cur = x
+    if chunks <= 1:
+        for _ in range(iters):
+            nxt = torch.empty_like(x)
+            ops.spmv(res.offsets, res.indices, cur, nxt[res.row_lo:res.row_hi])
+            works = [dist.broadcast(nxt[b[k]:b[k + 1]], src=src[k], group=group, async_op=True)
+                     for k in range(P) if b[k + 1] > b[k]]
+            for w in works:
+                w.wait()
+            cur = nxt
+        return cur
+    pieces = _spmv_pieces(res, chunks)
     for _ in range(iters):
         nxt = torch.empty_like(x)
-        ops.spmv(res.offsets, res.indices, cur, nxt[res.row_lo:res.row_hi])
-        works = [dist.broadcast(nxt[b[k]:b[k + 1]], src=dist.get_global_rank(group, k) if group else k,
-                                group=group, async_op=True) for k in range(P) if b[k + 1] > b[k]]
+        works = []
+        for c in range(chunks):
+            pc = pieces[c]
+            if pc is not None:
+                r0, r1, off_c, idx_c = pc
+                ops.spmv(off_c, idx_c, cur, nxt[res.row_lo + r0:res.row_lo + r1])
+            for k in range(P):
+                g0, g1 = _chunk_rows(b[k], b[k + 1], c, chunks)
+                if g1 > g0:
+                    works.append(dist.broadcast(nxt[g0:g1], src=src[k], group=group, async_op=True))
         for w in works:
             w.wait()
         cur = nxt
@@ -273,6 +339,17 @@ def shard_range(m_global: int, rank: int, world: int) -> tuple[int, int]:
     return e0, e0 + base + (1 if rank < extra else 0)
 
 
+def done_phases(evs, upto) -> set:
+    """Names of the phase marks recorded before event `upto` in `evs`."""
+    out = set()
+    for name, e in evs:
+        if e is upto:
+            break
+        if not name.startswith(("+", "-")):
+            out.add(name)
+    return out
+
+
 class ShardedPipeline:
     """The sharded pipeline of one rank on fixed shard geometry, with the
     timing hooks bench.py uses."""
@@ -289,43 +366,68 @@ class ShardedPipeline:
         return self.last
 
     def phase_times(self, I, J) -> dict:
-        """One step with CUDA events at the phase boundaries; ms per phase
-        (each includes its collectives), max over ranks."""
-        evs = {}
+        """One step with CUDA events at the phase boundaries and around every
+        collective: ms per phase (incl. its collectives), of which in
+        collectives ("comm_ms"), max over ranks; plus the step's compute-only,
+        comm-only and actual (overlapped) totals."""
+        evs = []
 
         def mark(name):
             e = torch.cuda.Event(enable_timing=True)
             e.record()
-            evs[name] = e
+            evs.append((name, e))
 
         self.run(I, J, mark)
         torch.cuda.synchronize()
-        names = ("start",) + self.PHASES
-        t = torch.tensor([evs[a].elapsed_time(evs[b]) for a, b in zip(names, names[1:])], dtype=torch.float64,
-                         device=self.device)
+        tot = {k: 0.0 for k in self.PHASES}
+        comm = {k: 0.0 for k in self.PHASES}
+        prev, c0 = evs[0][1], None
+        for name, e in evs[1:]:
+            if name == "+comm":
+                c0 = e
+            elif name == "-comm":
+                cur_comm = c0.elapsed_time(e)
+                phase = next(k for k in self.PHASES if k not in done_phases(evs, e))
+                comm[phase] += cur_comm
+            else:
+                tot[name] = prev.elapsed_time(e)
+                prev = e
+        vals = [tot[k] for k in self.PHASES] + [comm[k] for k in self.PHASES]
+        t = torch.tensor(vals, dtype=torch.float64, device=self.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
-        return {k: round(float(v), 4) for k, v in zip(self.PHASES, t.tolist())}
+        v = t.tolist()
+        K = len(self.PHASES)
+        out = {k: {"ms": round(v[i], 4), "comm_ms": round(v[K + i], 4), "compute_ms": round(v[i] - v[K + i], 4)}
+               for i, k in enumerate(self.PHASES)}
+        out["step"] = {"compute_only_ms": round(sum(v[i] - v[K + i] for i in range(K)), 4),
+                       "comm_only_ms": round(sum(v[K:]), 4), "actual_ms": round(sum(v[:K]), 4),
+                       "note": "collectives run on NCCL's stream; the step overlaps compute and comm only in "
+                               "P5 (sharded_spmv chunks)"}
+        return out
 
-    def spmv_timing(self, res: ShardResult, iters: int) -> dict:
+    def spmv_timing(self, res: ShardResult, iters: int, chunks: int = 1) -> dict:
         """P5: `iters` row-partitioned SpMV iterations (x = ones), ms per
-        iteration incl. the slice broadcasts, max over ranks."""
+        iteration incl. the slice broadcasts, max over ranks.  chunks > 1:
+        the broadcasts overlap the multiply piece by piece (sharded_spmv)."""
         x = torch.ones(self.n, dtype=torch.float32, device=self.device)
-        sharded_spmv(res, x, 1, self.group, self.ops)
+        sharded_spmv(res, x, 1, self.group, self.ops, chunks)
         torch.cuda.synchronize()
         dist.barrier(group=self.group)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        sharded_spmv(res, x, iters, self.group, self.ops)
+        sharded_spmv(res, x, iters, self.group, self.ops, chunks)
         b.record()
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64, device=self.device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         nnz = torch.tensor([res.indices.numel()], dtype=torch.float64, device=self.device)
         dist.all_reduce(nnz, op=dist.ReduceOp.MAX, group=self.group)
-        return {"iters": iters, "x": "ones", "ms_per_iter": round(float(t.item()), 4),
+        return {"iters": iters, "x": "ones", "chunks": chunks, "ms_per_iter": round(float(t.item()), 4),
                 "gedges_per_s": round(self.m / (float(t.item()) / 1e3) / 1e9, 3),
                 "max_rows_nnz_per_rank": int(nnz.item()), "balance": round(self.m / self.world / nnz.item(), 4),
-                "path": "owner rows x replicated x (boba_spmv), slices broadcast (allgather-v) per iteration"}
+                "path": "owner rows x replicated x (boba_spmv), slices broadcast (allgather-v) per iteration"
+                        + (f", {chunks} pieces per owner, each broadcast while the next is computed"
+                           if chunks > 1 else "")}
 
     @property
     def world(self) -> int:

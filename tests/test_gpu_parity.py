@@ -513,3 +513,31 @@ def test_pagerank_edge_cases(bb):
     for d in (0.0, 1.0, -0.5):
         with pytest.raises(ValueError):
             bb.pagerank(csr, damping=d)
+
+
+@pytest.mark.parametrize("scale,with_counts", [(18, True), (18, False), (22, True), (22, False)])
+def test_first_occurrence_seen_set_paths(dev, scale, with_counts):
+    """The two-stage sweep's SeenSet is filled from a counting prefix (most
+    frequent first-seen vertices first) when the caller's workspace has room
+    for the count table, and from the prefix's first-seen vertices otherwise
+    (boba_first_occurrence_shard with only the SeenSet workspace).  Both are
+    pure filters: first[] equals the reference's r either way.  s22 takes the
+    8-bit tags, s18 the 16-bit ones (reference _parallel.py:111-136)."""
+    import torch
+
+    from paper_2306_10410_b200 import _native as N
+
+    n = 1 << scale
+    I, J = dev.generate_rmat(scale, 16, seed=3)
+    lab = torch.from_numpy(oracle.random_labels(n, 9).astype(np.int32)).cuda()
+    I, J = dev.gather(lab, I), dev.gather(lab, J)
+    m = I.numel()
+    size = (N.lib.boba_first_occurrence_shard_workspace_size(n) if with_counts
+            else N.lib.boba_first_occurrence_workspace_size())
+    ws = torch.empty(size, dtype=torch.uint8, device="cuda")
+    first = torch.empty(n, dtype=torch.int32, device="cuda")
+    N.check(N.lib.boba_first_occurrence_shard(dev._p(I), dev._p(J), m, m, 0, n, dev._p(first), 0, dev._p(ws),
+                                              ws.numel(), dev._s()))
+    r, _ = oracle.first_hit_order_sequential(to_np(I), to_np(J), n)
+    want = np.where(r == oracle.RANK_UNSET, 0xFFFFFFFF, r).astype(np.uint32)
+    assert np.array_equal(to_np(first).astype(np.uint32), want)

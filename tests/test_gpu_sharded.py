@@ -161,8 +161,15 @@ def test_sharded_pipeline_one_rank_nccl(ops):
         small = native_sharded_reorder_to_csr(cu(I), cu(J), n, I.size, 0, recv_capacity=100)   # grows and retries
         assert np.array_equal(host(small.indices), idx)
         ph = sp.phase_times(cu(I), cu(J))
-        assert set(ph) == set(sp.PHASES) and all(v > 0 for v in ph.values())
+        assert set(ph) == set(sp.PHASES) | {"step"}
+        assert all(ph[k]["ms"] > 0 and 0 <= ph[k]["comm_ms"] <= ph[k]["ms"] for k in sp.PHASES)
+        assert ph["step"]["compute_only_ms"] + ph["step"]["comm_only_ms"] == pytest.approx(ph["step"]["actual_ms"],
+                                                                                            abs=1e-3)
         assert sp.spmv_timing(res, 2)["ms_per_iter"] > 0
+        # P5 with the slice exchange overlapped piece by piece: the same rows and sums
+        yc = sharded_spmv(res, torch.from_numpy(x).cuda(), 1, chunks=4).cpu().numpy()
+        np.testing.assert_allclose(yc, oracle.spmv_pull(off, idx, x.astype(np.float64)), rtol=1e-5, atol=0)
+        assert sp.spmv_timing(res, 2, chunks=4)["chunks"] == 4
         assert sp.comm_bytes()["total"] >= 0 and sp.kernel_launches_per_step() > 10
     finally:
         dist.destroy_process_group()
@@ -183,11 +190,12 @@ def _gpu_worker(rank, world, port, cases, outdir):
             res = sharded_reorder_to_csr(cu(I[e0:e1]), cu(J[e0:e1]), n, m, e0)
             x0 = torch.from_numpy((np.arange(n) % 7 + 1).astype(np.float32)).cuda()
             y2 = sharded_spmv(res, x0, 2)
+            y2c = sharded_spmv(res, x0, 2, chunks=3)   # exchange overlapped with the multiply
             torch.cuda.synchronize()
             np.savez(os.path.join(outdir, f"{name}_r{rank}.npz"), order=host(res.order), label=host(res.label),
                      I2=host(res.I2), J2=host(res.J2), lo=res.row_lo, hi=res.row_hi, offsets=host(res.offsets),
                      indices=host(res.indices), goff=res.row_edge_offset, bounds=np.array(res.bounds),
-                     y2=y2.cpu().numpy())
+                     y2=y2.cpu().numpy(), y2c=y2c.cpu().numpy())
     finally:
         dist.destroy_process_group()
 
@@ -218,3 +226,4 @@ def test_sharded_pipeline_ranks_share_one_gpu(ops, world, tmp_path):
         y = oracle.spmv_pull(off, idx, oracle.spmv_pull(off, idx, x))
         for p in parts:
             np.testing.assert_allclose(p["y2"], y, rtol=1e-5, atol=0)
+            np.testing.assert_allclose(p["y2c"], y, rtol=1e-5, atol=0)

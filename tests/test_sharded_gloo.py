@@ -130,10 +130,11 @@ def _worker(rank, world, port, cases, outdir):
         res = sharded_reorder_to_csr(t32(I[e0:e1]), t32(J[e0:e1]), n, m, e0, ops=ops)
         x0 = torch.from_numpy((np.arange(n) % 7 + 1).astype(np.float32))
         y2 = sharded_spmv(res, x0, 2, ops=ops)
+        y2c = sharded_spmv(res, x0, 2, ops=ops, chunks=3)   # exchange overlapped piece by piece
         np.savez(os.path.join(outdir, f"{name}_r{rank}.npz"), first=u32(res.first), order=u32(res.order),
                  label=u32(res.label), I2=u32(res.I2), J2=u32(res.J2), lo=res.row_lo, hi=res.row_hi,
                  offsets=u32(res.offsets), indices=u32(res.indices), goff=res.row_edge_offset,
-                 bounds=np.array(res.bounds), y2=y2.numpy())
+                 bounds=np.array(res.bounds), y2=y2.numpy(), y2c=y2c.numpy())
     dist.destroy_process_group()
 
 
@@ -190,6 +191,7 @@ def test_sharded_pipeline_matches_oracle(world, tmp_path):
         y = oracle.spmv_pull(off, idx, oracle.spmv_pull(off, idx, x))
         for p in parts:
             np.testing.assert_allclose(p["y2"], y, rtol=1e-5, atol=0)
+            assert np.array_equal(p["y2c"], p["y2"])   # same rows, same sums: chunking changes only the schedule
         if name == "rmat":   # the edge-balanced cut actually balances
             sizes = [int(off[p["hi"]] - off[p["lo"]]) for p in parts]
             assert max(sizes) <= 1.5 * I.size / world + 64, sizes

@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 PHASES = [
-    ("first_occurrence", ("k_first_hit", "k_seen_build")),
+    ("first_occurrence", ("k_first_hit", "k_seen_build", "k_merge_bits", "k_prefix_count")),
     ("compact", ("k_mark", "k_sector_scan", "k_assign", "k_hub_labels")),
     ("relabel", ("k_relabel",)),
     ("coo_to_csr", ("k_set_u32", "k_radix_", "k_scan_u32", "k_suffix_min", "k_row_starts")),
