@@ -1,7 +1,8 @@
 """A/B of COO->CSR variants on the bench graphs: times boba_coo_to_csr under
 each BOBA_RADIX setting (CUDA events, L2 flushed, median of R) and checks every
 variant's offsets/indices bit for bit against the first one.
-usage: csr_ab.py CFG[,CFG...] [R] [variants]   CFG in c2 c3 c5 c4 sNN; variants e.g. "1,2"."""
+usage: csr_ab.py CFG[,CFG...] [R] [variants]   CFG in c2 c3 c5 c4 sNN; variants: comma-separated
+ENV=value settings applied in turn (e.g. "BOBA_CSR_MAXBITS=8,BOBA_CSR_MAXBITS=9"), or bare labels."""
 import os
 import sys
 
@@ -29,7 +30,7 @@ def graph(cfg):
 def main():
     cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c2"]
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-    variants = sys.argv[3].split(",") if len(sys.argv) > 3 else ["1", "2"]
+    variants = sys.argv[3].split(",") if len(sys.argv) > 3 else ["default"]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for cfg in cfgs:
         I, J, n = graph(cfg)
@@ -39,7 +40,9 @@ def main():
         del I, J
         ref = None
         for v in variants:
-            os.environ["BOBA_RADIX"] = v
+            if "=" in v:
+                k, val = v.split("=", 1)
+                os.environ[k] = val
             ws = torch.empty(N.lib.boba_coo_to_csr_workspace_size(m, n, 0), dtype=torch.uint8, device="cuda")
             offsets = torch.empty(n + 1, dtype=torch.int32, device="cuda")
             indices = torch.empty(m, dtype=torch.int32, device="cuda")
@@ -61,7 +64,7 @@ def main():
                 same = bool(torch.equal(ref[0], offsets) and torch.equal(ref[1], indices))
             alg = 16 * m + 4 * n + 4
             med = float(np.median(ts))
-            print(f"{cfg} n={n} m={m} BOBA_RADIX={v}: median {med:.4f} ms min {min(ts):.4f} "
+            print(f"{cfg} n={n} m={m} [{v}]: median {med:.4f} ms min {min(ts):.4f} "
                   f"({alg / med / 1e6:.0f} GB/s alg) same={same}", flush=True)
             del ws
         del pipe, ref

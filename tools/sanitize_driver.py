@@ -5,7 +5,9 @@ weighted CSR, SpMV fp32/fp64 (vector and scalar staging), PageRank, degree /
 hub orders, destination sort, NBR, the multi-GPU ops (windowed compaction,
 row cut, relative range partition) and the host transfers.  Argument
 "waves": instead, one pipeline at n = 2^25 (wave-guarded first occurrence,
-range-pass relabel)."""
+range-pass relabel with the fused first radix histogram).  The default run
+also takes one s17 graph through the two-stage first occurrence (counting
+prefix, frequency-ordered SeenSet fill)."""
 import os
 import sys
 
@@ -19,6 +21,7 @@ from paper_2306_10410_b200 import device as D  # noqa: E402
 from paper_2306_10410_b200.sharded import DeviceOps  # noqa: E402
 
 if len(sys.argv) > 1 and sys.argv[1] == "waves":
+    os.environ["BOBA_RL_PASSES"] = "2"   # range-pass relabel, the last pass writing the first radix histogram
     scale = 25
     I, J = D.generate_rmat(scale, 1, 3)
     n = 1 << scale
@@ -28,6 +31,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "waves":
     print("waves ok")
     sys.exit(0)
 
+# two-stage first occurrence with the counting prefix (m >= 16 x 64K)
+I, J = D.generate_rmat(17, 16, 2)
+D.Pipeline(I.numel(), 1 << 17).run(I, J)
 scale = 14
 n = 1 << scale
 I, J = D.generate_rmat(scale, 8, 1)
