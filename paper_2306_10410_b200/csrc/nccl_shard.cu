@@ -194,7 +194,8 @@ int boba_sharded_reorder_to_csr_nccl(const uint32_t* I, const uint32_t* J, uint6
     }
     NK(api.group_end());
     // the partition needs only the device-side bounds: queue it before the host sync
-    if (m_local)
+    // (one rank: the shard already is the owner's edges in edge order)
+    if (m_local && P > 1)
         CK(launch_range_partition(I2, J2, m_local, W.cut, P, W.keys, W.vals, nullptr, W.pw, W.pw_bytes, sms, s,
                                   true));
     std::vector<uint32_t> h(4 * P + 2);
@@ -216,6 +217,12 @@ int boba_sharded_reorder_to_csr_nccl(const uint32_t* I, const uint32_t* J, uint6
     if (total > recv_capacity)
         return boba_sharded_fail(BOBA_EINVAL, what, "recv_capacity too small (out->nnz holds the need)");
     // all-to-all of rows and of columns in rank order
+    const uint32_t* ck = W.rk;
+    const uint32_t* cv = W.rv;
+    if (P == 1) {
+        ck = I2;
+        cv = J2;
+    } else {
     NK(api.group_start());
     uint64_t so = 0, ro = 0;
     for (int k = 0; k < P; k++) {
@@ -231,10 +238,11 @@ int boba_sharded_reorder_to_csr_nccl(const uint32_t* I, const uint32_t* J, uint6
         ro += recvd[k];
     }
     NK(api.group_end());
+    }
     // the owner's stable CSR over rows [row_lo, row_hi) (keys arrive relative to row_lo)
     const uint32_t rows = out->row_hi - out->row_lo;
-    CK(launch_coo_to_csr(W.rk, W.rv, nullptr, total, rows, nullptr, offsets, indices, nullptr, W.csr, W.csr_bytes,
-                         sms, s));
+    CK(launch_coo_to_csr(ck, cv, nullptr, total, rows, nullptr, offsets, indices, nullptr, W.csr, W.csr_bytes, sms,
+                         s));
 #undef CK
 #undef NK
     return BOBA_OK;
