@@ -27,6 +27,7 @@
 #include "hubs.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace boba {
@@ -349,8 +350,8 @@ size_t first_hit_bits_workspace_bytes(uint32_t n) {
     return bits > kCountBytes ? bits : kCountBytes;
 }
 
-// Static sweep of r in waves of kFhWave positions (BITS mode, see sweep_static).
-constexpr uint64_t kFhWaveQuads = (1ull << 26) / 4;
+// Static sweep of r in waves of positions (BITS mode, see sweep_static).
+constexpr uint64_t kFhWaveQuads0 = (1ull << 22) / 4, kFhWaveQuadsMax = (1ull << 30) / 4;
 
 template <int TW>
 static cudaError_t launch_static_waves(const Ranges& r, uint32_t* first, const uint32_t* set,
@@ -363,8 +364,15 @@ static cudaError_t launch_static_waves(const Ranges& r, uint32_t* first, const u
     if (e != cudaSuccess) return e;
     const uint64_t total = r.qa + r.qb;
     const uint64_t mb = ceil_div(words, 256), cap = (uint64_t)num_sms * 8;
-    for (uint64_t w0 = 0; w0 < total; w0 += kFhWaveQuads) {
-        const uint64_t w1 = w0 + kFhWaveQuads < total ? w0 + kFhWaveQuads : total;
+    // Geometric waves: 2^22 positions, doubling up to 2^30.  A wave costs a
+    // red.min for every position whose vertex is unseen before the wave, so
+    // early in the stream (nearly every vertex new) short waves move vertices
+    // into the bitmap sooner; later waves are nearly all bitmap hits and long
+    // ones save merges.  Measured at s26: fixed 2^26-position waves 8.64 ms,
+    // geometric 2^22 -> 2^26 7.73, 2^22 -> 2^28 7.26, 2^22 -> 2^30 7.22.
+    uint64_t wq = kFhWaveQuads0;
+    for (uint64_t w0 = 0; w0 < total; w0 += wq, wq = wq * 2 < kFhWaveQuadsMax ? wq * 2 : kFhWaveQuadsMax) {
+        const uint64_t w1 = w0 + wq < total ? w0 + wq : total;
         Ranges rw{};
         const uint64_t a0 = w0 < r.qa ? w0 : r.qa, a1 = w1 < r.qa ? w1 : r.qa;  // part in A
         rw.a = r.a + 4 * a0;
