@@ -68,7 +68,7 @@ int boba_first_occurrence(const uint32_t *I, const uint32_t *J, uint64_t m, uint
  * enables the two-stage sweep with the shared-memory SeenSet of hubs; with
  * boba_first_occurrence_shard_workspace_size(n) bytes, also the prefix count
  * table that fills the SeenSet with the most frequent vertices first, and the
- * wave-guarded sweep the fused single-GPU call uses beyond L2 (n > 2^24). */
+ * wave-guarded sweep the fused single-GPU call uses beyond L2 (n > 2^23). */
 size_t boba_first_occurrence_workspace_size(void);
 size_t boba_first_occurrence_shard_workspace_size(uint32_t n);
 int boba_first_occurrence_shard(const uint32_t *I, const uint32_t *J, uint64_t m_local,

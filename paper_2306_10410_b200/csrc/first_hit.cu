@@ -426,9 +426,10 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
                 k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, 1u, set);
             };
             Ranges r2{I + prefix, quads - qp, base_i + prefix, J, quads, base_j};
-            // first[] beyond L2 (n > 2^24, > 64 MB): guard on a seen-bitmap in waves instead of
-            // first[] itself (measured: s26 18.0 -> 9.3 ms; s24, table still partly in L2: 1.90 vs 2.35)
-            const bool waves = bits_ws && n > (1u << 24);
+            // first[] beyond L2 (n > 2^23, > 32 MB): guard on a seen-bitmap in geometric waves
+            // instead of first[] itself (measured: s26 18.0 -> 7.2 ms; s24 1.70 -> 1.66; s22, first[]
+            // L2-resident, 0.32 -> 0.44, so not there)
+            const bool waves = bits_ws && n > (1u << 23);
             if (hh.tag_bits <= 8) {
                 build(std::integral_constant<int, 8>{});
                 if (waves) err = launch_static_waves<8>(r2, first, set, hh, n, bits_ws, num_sms, s);

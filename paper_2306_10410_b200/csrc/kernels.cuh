@@ -12,7 +12,7 @@ cudaError_t launch_first_hit(const uint32_t* I, const uint32_t* J, uint64_t m, u
 
 // seen_ws (first_hit_workspace_bytes(), may be NULL) enables the two-stage sweep
 size_t first_hit_workspace_bytes();
-// bits_ws (first_hit_bits_workspace_bytes(n), may be NULL): for n > 2^24 the
+// bits_ws (first_hit_bits_workspace_bytes(n), may be NULL): for n > 2^23 the
 // two-stage sweep then guards on an L2-resident seen-bitmap in waves
 size_t first_hit_bits_workspace_bytes(uint32_t n);
 cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_t m, uint64_t m_global, uint64_t e0,

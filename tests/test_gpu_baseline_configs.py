@@ -14,9 +14,11 @@ is checked against the oracle's fp64 row sums within rtol 1e-5 on a seeded
 U[0,1) vector.
 
 These exercise the size-dependent code paths no small case reaches: the
-8-bit SeenSet tags (s22), the 16-bit static sweep without waves and the
-no-hub-table relabel (n = 2^24), the wave-guarded first-occurrence sweep and
-the two range passes of relabel (s26), 3 and 4 radix passes.
+8-bit SeenSet tags (s22), the 16-bit wave-guarded sweep and the no-hub-table
+relabel (n = 2^24), the geometric waves up to 2^30 positions and the two
+range passes of relabel with the fused first radix histogram (s26), 3 and 4
+radix passes.  (The 16-bit sweep without waves, n in (2^22, 2^23], is
+test_gpu_parity.py::test_sixteen_bit_static_sweep_without_waves.)
 """
 
 import os

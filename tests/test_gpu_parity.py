@@ -541,3 +541,18 @@ def test_first_occurrence_seen_set_paths(dev, scale, with_counts):
     r, _ = oracle.first_hit_order_sequential(to_np(I), to_np(J), n)
     want = np.where(r == oracle.RANK_UNSET, 0xFFFFFFFF, r).astype(np.uint32)
     assert np.array_equal(to_np(first).astype(np.uint32), want)
+
+
+def test_sixteen_bit_static_sweep_without_waves(dev):
+    """n = 2^23: SeenSet tags are 16-bit (ids wider than 2^22) and first[]
+    (32 MB) still guards the sweep directly -- no waves (those start above
+    2^23).  The whole pipeline against the oracle (reference
+    _parallel.py:111-136, graph.py:253-289)."""
+    import torch
+
+    scale = 23
+    n = 1 << scale
+    I, J = dev.generate_rmat(scale, 4, seed=4)
+    lab = torch.from_numpy(oracle.random_labels(n, 11).astype(np.int32)).cuda()
+    I, J = dev.gather(lab, I), dev.gather(lab, J)
+    pipeline_vs_oracle(dev, I, J, n)
