@@ -1,5 +1,7 @@
 #!/bin/sh
-# ncu --set full of one launch of each c4 hot kernel (tools/profile_step.py 26 1), report in gpurun_out/
-K='regex:k_radix_downsweep|k_relabel_range|k_first_hit_static|k_assign|k_spmv_merge|k_radix_upsweep|k_mark'
-ncu --set full --clock-control none --import-source on -k "$K" --launch-count 12 -o gpurun_out/r02_c4_full python tools/profile_step.py 26 1 > gpurun_out/r02_c4_full.log 2>&1
-echo "ncu rc=$?"
+# ncu --set full of the first launch of each c4 hot kernel (tools/profile_step.py 26 1); reports in gpurun_out/
+for k in k_radix_downsweep k_radix_upsweep k_relabel_range k_first_hit_static k_assign k_mark k_spmv_merge; do
+  ncu --set full --clock-control none --import-source on -k "regex:$k" --launch-count 1 -o gpurun_out/r02_c4_$k \
+      python tools/profile_step.py 26 1 > gpurun_out/r02_c4_$k.log 2>&1
+  echo "$k rc=$?"
+done
