@@ -114,6 +114,19 @@ size_t boba_coo_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted);
 int boba_coo_to_csr(const uint32_t *I2, const uint32_t *J2, const double *weights, uint64_t m,
                     uint32_t n, const uint32_t *row_counts, uint32_t *offsets, uint32_t *indices,
                     double *weights_out, void *workspace, size_t workspace_bytes, void *stream);
+/* The same conversion in two steps, so the row keys can be histogrammed while
+ * the columns are still in flight (the multi-GPU owner overlaps its column
+ * all-to-all this way): boba_coo_to_csr_first_hist(I2, ...) writes the first
+ * radix pass's tile histogram into the workspace; a following
+ * boba_coo_to_csr_ex(..., first_hist_ready = 1, ...) with the same I2, m, n
+ * and workspace skips that pass's upsweep (row_counts must be NULL then).
+ * Same results as boba_coo_to_csr. */
+int boba_coo_to_csr_first_hist(const uint32_t *I2, uint64_t m, uint32_t n, void *workspace,
+                               size_t workspace_bytes, void *stream);
+int boba_coo_to_csr_ex(const uint32_t *I2, const uint32_t *J2, const double *weights, uint64_t m,
+                       uint32_t n, const uint32_t *row_counts, uint32_t *offsets, uint32_t *indices,
+                       double *weights_out, void *workspace, size_t workspace_bytes,
+                       int first_hist_ready, void *stream);
 
 /* --- Phase 5: SpMV (fp32) -------------------------------------------------
  * y[v] = sum over row v of weights[k] * x[indices[k]] (weights NULL = 1);

@@ -49,6 +49,8 @@ SIGNATURES = {
     "boba_degrees": ([_P, _U64, _U32, _P, _P], _I),
     "boba_coo_to_csr_workspace_size": ([_U64, _U32, _I], _SZ),
     "boba_coo_to_csr": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _SZ, _P], _I),
+    "boba_coo_to_csr_ex": ([_P, _P, _P, _U64, _U32, _P, _P, _P, _P, _P, _SZ, _I, _P], _I),
+    "boba_coo_to_csr_first_hist": ([_P, _U64, _U32, _P, _SZ, _P], _I),
     "boba_spmv_workspace_size": ([_U32, _U64], _SZ),
     "boba_spmv": ([_P, _P, _P, _P, _P, _U32, _U64, _P, _SZ, _P], _I),
     "boba_spmv_f64": ([_P, _P, _P, _P, _P, _U32, _U64, _P, _SZ, _P], _I),

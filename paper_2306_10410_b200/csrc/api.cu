@@ -232,16 +232,32 @@ size_t boba_coo_to_csr_workspace_size(uint64_t m, uint32_t n, int weighted) {
     return boba::coo_to_csr_workspace_bytes(m, n, weighted != 0);
 }
 
-int boba_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
-                    const uint32_t* row_counts, uint32_t* offsets, uint32_t* indices, double* w_out, void* ws,
-                    size_t ws_bytes, void* stream) {
+int boba_coo_to_csr_ex(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
+                       const uint32_t* row_counts, uint32_t* offsets, uint32_t* indices, double* w_out, void* ws,
+                       size_t ws_bytes, int first_hist_ready, void* stream) {
     if (int rc = check_sizes(m, n, "boba_coo_to_csr")) return rc;
     REQUIRE(offsets && ws, "boba_coo_to_csr: NULL offsets/workspace");
     REQUIRE((I2 && J2 && indices) || m == 0, "boba_coo_to_csr: NULL edge arrays");
     REQUIRE(!w || w_out || m == 0, "boba_coo_to_csr: weights given but weights_out is NULL");
+    REQUIRE(!first_hist_ready || !row_counts, "boba_coo_to_csr_ex: first_hist_ready with row_counts");
     return cuda_status(boba::launch_coo_to_csr(I2, J2, w, m, n, row_counts, offsets, indices, w_out, ws, ws_bytes,
-                                               num_sms(), S(stream)),
+                                               num_sms(), S(stream), first_hist_ready != 0),
                        "boba_coo_to_csr");
+}
+
+int boba_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
+                    const uint32_t* row_counts, uint32_t* offsets, uint32_t* indices, double* w_out, void* ws,
+                    size_t ws_bytes, void* stream) {
+    return boba_coo_to_csr_ex(I2, J2, w, m, n, row_counts, offsets, indices, w_out, ws, ws_bytes, 0, stream);
+}
+
+int boba_coo_to_csr_first_hist(const uint32_t* I2, uint64_t m, uint32_t n, void* ws, size_t ws_bytes, void* stream) {
+    if (int rc = check_sizes(m, n, "boba_coo_to_csr_first_hist")) return rc;
+    REQUIRE(ws, "boba_coo_to_csr_first_hist: NULL workspace");
+    REQUIRE(I2 || m == 0, "boba_coo_to_csr_first_hist: NULL rows");
+    REQUIRE(ws_bytes >= boba::coo_to_csr_workspace_bytes(m, n, false), "boba_coo_to_csr_first_hist: workspace too small");
+    return cuda_status(boba::launch_coo_to_csr_first_hist(I2, m, n, ws, ws_bytes, num_sms(), S(stream)),
+                       "boba_coo_to_csr_first_hist");
 }
 
 size_t boba_spmv_workspace_size(uint32_t n, uint64_t m) { return boba::spmv_workspace_bytes(n, m); }

@@ -312,6 +312,23 @@ cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int
 
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool /*weighted*/) { return carve(nullptr, m, n).total; }
 
+// The first radix pass's tile histogram alone (its upsweep), into the
+// workspace launch_coo_to_csr(..., first_hist_ready = true) reads it from: a
+// caller can run it as soon as the row keys exist, e.g. while the columns are
+// still arriving over the network (sharded.py, nccl_shard.cu).
+cudaError_t launch_coo_to_csr_first_hist(const uint32_t* I2, uint64_t m, uint32_t n, void* ws, size_t ws_bytes,
+                                         int num_sms, cudaStream_t s) {
+    const CsrPlan p = plan_for(n);
+    const CsrWs W = carve(ws, m, n);
+    if (ws_bytes < W.total) return cudaErrorInvalidValue;
+    if (p.passes == 0 || m == 0) return cudaSuccess;
+    const uint64_t tiles = ceil_div(m, p.tile);
+    const uint64_t up_grid = tiles < (uint64_t)num_sms * 8 ? tiles : (uint64_t)num_sms * 8;
+    const DigitShift op{p.shift[0], (1u << p.bits[0]) - 1u};
+    k_radix_upsweep<8, 256, 16, DigitShift><<<(unsigned)up_grid, 256, 0, s>>>(I2, m, op, p.bits[0], tiles, W.H);
+    return cudaGetLastError();
+}
+
 RowTileHist coo_to_csr_first_hist(void* ws, size_t ws_bytes, uint64_t m, uint32_t n, bool /*weighted*/) {
     RowTileHist r;
     const CsrPlan p = plan_for(n);

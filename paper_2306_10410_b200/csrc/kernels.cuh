@@ -35,6 +35,9 @@ struct RowTileHist {
     bool done = false;      // set by launch_relabel when it wrote H
 };
 RowTileHist coo_to_csr_first_hist(void* ws, size_t ws_bytes, uint64_t m, uint32_t n, bool weighted);
+// the same histogram computed on its own from the row keys
+cudaError_t launch_coo_to_csr_first_hist(const uint32_t* I2, uint64_t m, uint32_t n, void* ws, size_t ws_bytes,
+                                         int num_sms, cudaStream_t s);
 
 // counts (may be NULL): also the out-degree histogram of the new rows
 cudaError_t launch_relabel(const uint32_t* I, const uint32_t* J, uint64_t m, const uint32_t* label,

@@ -8,8 +8,10 @@
 //       (_parallel.py:178-201), order = inverse of label
 //   P3  relabel of the shard with the hub table (graph.py:280-289)
 //   P4  coarse row histogram allreduce-SUM, row cut, stable relative range
-//       partition, all-to-all of (row, col) by grouped send/recv in rank
-//       order, the owner's stable COO->CSR (graph.py:253-277)
+//       partition, all-to-all of the rows and then of the columns by grouped
+//       send/recv in rank order on a side stream, the owner's first radix
+//       histogram of the rows overlapping the column exchange, its stable
+//       COO->CSR (graph.py:253-277)
 // One host synchronisation per call (the row bounds and the send / receive
 // counts the grouped send/recv need).
 //
@@ -216,33 +218,54 @@ int boba_sharded_reorder_to_csr_nccl(const uint32_t* I, const uint32_t* J, uint6
         for (int k = 0; k <= P; k++) bounds_host[k] = bounds[k];
     if (total > recv_capacity)
         return boba_sharded_fail(BOBA_EINVAL, what, "recv_capacity too small (out->nnz holds the need)");
-    // all-to-all of rows and of columns in rank order
+    // all-to-all of rows, then of columns, in rank order, on a side stream:
+    // the owner histograms the rows for its first radix pass while the
+    // columns are still in flight
+    const uint32_t rows = out->row_hi - out->row_lo;
     const uint32_t* ck = W.rk;
     const uint32_t* cv = W.rv;
+    bool hist_ready = false;
     if (P == 1) {
         ck = I2;
         cv = J2;
     } else {
-    NK(api.group_start());
-    uint64_t so = 0, ro = 0;
-    for (int k = 0; k < P; k++) {
-        if (sent[k]) {
-            NK(api.send(W.keys + so, sent[k], ncclUint32, k, comm, s));
-            NK(api.send(W.vals + so, sent[k], ncclUint32, k, comm, s));
+        cudaStream_t cs = nullptr;
+        cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // partition done, rows in, columns in
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        struct Release {
+            cudaStream_t& cs;
+            cudaEvent_t* ev;
+            ~Release() {
+                for (int i = 0; i < 3; i++)
+                    if (ev[i]) cudaEventDestroy(ev[i]);
+                if (cs) cudaStreamDestroy(cs);
+            }
+        } release{cs, ev};
+        for (auto& evt : ev) CK(cudaEventCreateWithFlags(&evt, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev[0], s));
+        CK(cudaStreamWaitEvent(cs, ev[0], 0));
+        for (int pass = 0; pass < 2; pass++) {
+            const uint32_t* src = pass == 0 ? W.keys : W.vals;
+            uint32_t* dst = pass == 0 ? W.rk : W.rv;
+            NK(api.group_start());
+            uint64_t so = 0, ro = 0;
+            for (int k = 0; k < P; k++) {
+                if (sent[k]) NK(api.send(src + so, sent[k], ncclUint32, k, comm, cs));
+                if (recvd[k]) NK(api.recv(dst + ro, recvd[k], ncclUint32, k, comm, cs));
+                so += sent[k];
+                ro += recvd[k];
+            }
+            NK(api.group_end());
+            CK(cudaEventRecord(ev[1 + pass], cs));
         }
-        if (recvd[k]) {
-            NK(api.recv(W.rk + ro, recvd[k], ncclUint32, k, comm, s));
-            NK(api.recv(W.rv + ro, recvd[k], ncclUint32, k, comm, s));
-        }
-        so += sent[k];
-        ro += recvd[k];
-    }
-    NK(api.group_end());
+        CK(cudaStreamWaitEvent(s, ev[1], 0));
+        CK(launch_coo_to_csr_first_hist(W.rk, total, rows, W.csr, W.csr_bytes, sms, s));
+        CK(cudaStreamWaitEvent(s, ev[2], 0));
+        hist_ready = true;
     }
     // the owner's stable CSR over rows [row_lo, row_hi) (keys arrive relative to row_lo)
-    const uint32_t rows = out->row_hi - out->row_lo;
     CK(launch_coo_to_csr(ck, cv, nullptr, total, rows, nullptr, offsets, indices, nullptr, W.csr, W.csr_bytes, sms,
-                         s));
+                         s, hist_ready));
 #undef CK
 #undef NK
     return BOBA_OK;

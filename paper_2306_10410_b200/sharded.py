@@ -24,7 +24,9 @@ of P holds edges [e0, e0 + ml) of the m-edge list, in order, i.e. positions
       cols, and the owner's stable COO->CSR of what it received.  Senders are
       ranks in order and shards are contiguous in edge order, so the received
       sequence is global edge order restricted to the owner's rows: the
-      reference's within-row order (_parallel.py:55-88), bit-exact.
+      reference's within-row order (_parallel.py:55-88), bit-exact.  The rows
+      are exchanged before the columns, and the owner computes its first radix
+      histogram of the rows while the columns are in flight.
   P5  row-partitioned SpMV (kernels.py:30-52): the owner multiplies its rows
       by the replicated x; between iterations every owner broadcasts its y
       slice (an allgather-v) into the next x.
@@ -123,6 +125,22 @@ class DeviceOps:
         offsets, indices, _ = D.coo_to_csr(rows, cols, n_rows)
         return offsets, indices
 
+    def coo_to_csr_begin(self, rows, n_rows: int):
+        """The first radix pass's tile histogram of the row keys alone
+        (boba_coo_to_csr_first_hist); -> the workspace holding it."""
+        m = rows.numel()
+        ws = D._ws(N.lib.boba_coo_to_csr_workspace_size(m, n_rows, 0), rows.device)
+        N.check(N.lib.boba_coo_to_csr_first_hist(D._p(rows), m, n_rows, D._p(ws), ws.numel(), D._s()))
+        return ws
+
+    def coo_to_csr_finish(self, ws, rows, cols, n_rows: int):
+        """The rest of the conversion, reusing that histogram."""
+        m = rows.numel()
+        offsets, indices = _e(n_rows + 1, rows.device), _e(m, rows.device)
+        N.check(N.lib.boba_coo_to_csr_ex(D._p(rows), D._p(cols), None, m, n_rows, None, D._p(offsets),
+                                         D._p(indices), None, D._p(ws), ws.numel(), 1, D._s()))
+        return offsets, indices
+
     def spmv(self, offsets, indices, x, out):
         return D.spmv(offsets, indices, x, out=out)
 
@@ -144,10 +162,11 @@ class ShardResult:
     received: list            # edges this rank received from each sender
 
 
-def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int], group=None) -> torch.Tensor:
+def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int], group=None, async_op=False):
     recv = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
-    dist.all_to_all_single(recv, send, output_split_sizes=recv_counts, input_split_sizes=send_counts, group=group)
-    return recv
+    work = dist.all_to_all_single(recv, send, output_split_sizes=recv_counts, input_split_sizes=send_counts,
+                                  group=group, async_op=async_op)
+    return (recv, work) if async_op else recv
 
 
 def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: int, e0: int, group=None,
@@ -202,17 +221,25 @@ def sharded_reorder_to_csr(I: torch.Tensor, J: torch.Tensor, n: int, m_global: i
     goff = meta[P + 1:2 * P + 2]
     sent = meta[2 * P + 2:3 * P + 2]
     received = meta[3 * P + 2:]
+    lo, hi = bounds[r], bounds[r + 1]
     if P == 1:   # one owner: the shard is already the owner's edges in edge order
-        rk, rv = I2, J2
+        offsets, indices = ops.coo_to_csr(I2, J2, hi - lo)
     else:
         keys, vals = ops.range_partition(I2, J2, cut[:P + 1], P)
+        # rows first, then columns (both queued on the collective's stream); the
+        # owner histograms the rows for its first radix pass while the columns
+        # are still in flight
         mark("+comm")
-        rk = _alltoallv(keys, sent, received, group)
-        rv = _alltoallv(vals, sent, received, group)
+        rk, wk = _alltoallv(keys, sent, received, group, async_op=True)
+        rv, wv = _alltoallv(vals, sent, received, group, async_op=True)
+        wk.wait()
+        mark("-comm")
+        state = ops.coo_to_csr_begin(rk, hi - lo)
+        mark("+comm")
+        wv.wait()
         mark("-comm")
         del keys, vals
-    lo, hi = bounds[r], bounds[r + 1]
-    offsets, indices = ops.coo_to_csr(rk, rv, hi - lo)
+        offsets, indices = ops.coo_to_csr_finish(state, rk, rv, hi - lo)
     mark("coo_to_csr")
     return ShardResult(first, order, label, I2, J2, lo, hi, offsets, indices, goff[r], bounds, sent, received)
 
@@ -401,8 +428,8 @@ class ShardedPipeline:
                for i, k in enumerate(self.PHASES)}
         out["step"] = {"compute_only_ms": round(sum(v[i] - v[K + i] for i in range(K)), 4),
                        "comm_only_ms": round(sum(v[K:]), 4), "actual_ms": round(sum(v[:K]), 4),
-                       "note": "collectives run on NCCL's stream; the step overlaps compute and comm only in "
-                               "P5 (sharded_spmv chunks)"}
+                       "note": "collectives run on NCCL's stream; compute overlaps them in P4 (the owner's row "
+                               "histogram while the columns arrive) and in P5 (sharded_spmv chunks)"}
         return out
 
     def spmv_timing(self, res: ShardResult, iters: int, chunks: int = 1) -> dict:

@@ -124,6 +124,13 @@ def test_row_cut_and_relative_partition(ops, n):
     ko, vo = ops.range_partition(cu(local), cu(cols), cut[:P + 1], P)
     wk, wv = npo.range_partition(t32(local), t32(cols), t32(b), P)
     assert np.array_equal(host(ko), u32(wk)) and np.array_equal(host(vo), u32(wv))
+    # the owner's two-step CSR (row histogram first, while the columns arrive) == one call == numpy
+    want_off, want_idx = npo.coo_to_csr(t32(local), t32(cols), n)
+    st = ops.coo_to_csr_begin(cu(local), n)
+    o2, i2 = ops.coo_to_csr_finish(st, cu(local), cu(cols), n)
+    o1, i1 = ops.coo_to_csr(cu(local), cu(cols), n)
+    assert np.array_equal(host(o2), u32(want_off)) and np.array_equal(host(i2), u32(want_idx))
+    assert np.array_equal(host(o1), host(o2)) and np.array_equal(host(i1), host(i2))
 
 
 def test_sharded_pipeline_one_rank_nccl(ops):

@@ -108,6 +108,12 @@ class NumpyOps:
         off = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=n_rows))])
         return t32(off), t32(c[o])
 
+    def coo_to_csr_begin(self, rows, n_rows):
+        return None
+
+    def coo_to_csr_finish(self, state, rows, cols, n_rows):
+        return self.coo_to_csr(rows, cols, n_rows)
+
     def spmv(self, offsets, indices, x, out):
         off, idx = u32(offsets).astype(np.int64), u32(indices).astype(np.int64)
         xs = x.numpy().astype(np.float64)
