@@ -1,8 +1,9 @@
-"""A/B of COO->CSR variants on the bench graphs: times boba_coo_to_csr under
-each BOBA_RADIX setting (CUDA events, L2 flushed, median of R) and checks every
-variant's offsets/indices bit for bit against the first one.
-usage: csr_ab.py CFG[,CFG...] [R] [variants]   CFG in c2 c3 c5 c4 sNN; variants: comma-separated
-ENV=value settings applied in turn (e.g. "BOBA_CSR_MAXBITS=8,BOBA_CSR_MAXBITS=9"), or bare labels."""
+"""A/B of COO->CSR variants on the bench graphs: times boba_coo_to_csr (CUDA
+events, L2 flushed, median of R) once per variant and checks every variant's
+offsets/indices bit for bit against the first one.  A variant is an ENV=value
+setting read by the library (e.g. BOBA_RL_PASSES) or a bare label (to compare
+library builds run one after another with BOBA_LIB_PATH).
+usage: csr_ab.py CFG[,CFG...] [R] [variants]   CFG in c2 c3 c5 c4 sNN"""
 import os
 import sys
 
