@@ -33,7 +33,10 @@
 namespace boba {
 
 constexpr int kFhNT = 1024;              // threads per CTA (one CTA per SM)
-constexpr int kFhQuads = 4;              // 16-byte quads per thread per iteration
+// 16-byte quads per thread per iteration (measured, static sweep, c4 / c5 /
+// c3 / c2: 4 quads 7.24 / 1.656 / 0.830 / 0.323 ms, 2 quads 7.19 / 1.627 /
+// 0.811 / 0.322, 1 quad 7.17 / 1.621 / 0.797 / 0.348, 8 quads 12.1 / 2.89)
+constexpr int kFhQuads = 2;
 constexpr int kFhSlotsLog2 = 15;         // 32K-slot finalised-vertex set (128 KB), dynamic mode
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
