@@ -253,8 +253,10 @@ __global__ void k_merge_bits(uint32_t* seenb, uint32_t* newb, uint64_t words) {
 
 // SeenSet from the counting prefix: a vertex whose first occurrence is one of
 // the prefix positions (exactly one thread per vertex) and whose prefix count
-// reaches `thr` gets its tag into a free lane of its bucket.  Two rounds
-// (frequent vertices first, then any) fill the lanes in priority order; a
+// reaches `thr` gets its tag into a free lane of its bucket.  Rounds of
+// decreasing threshold (frequent vertices first, then any) fill the lanes in
+// priority order (measured at s26: rounds 8 / 4 / 1 6.99 ms, 4 / 1 7.19,
+// 8 / 1 7.01, 2 / 1 7.80; at s22 the extra round costs more than it saves); a
 // full bucket drops the vertex: membership only ever saves work, it never
 // changes first[].  Without counts (cnt == NULL) every such vertex is offered.
 template <int TW>
@@ -425,6 +427,9 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
             }
             auto build = [&](auto tw) {
                 constexpr int TW = decltype(tw)::value;
+                // fill rounds, most frequent first: counts >= 8 (wide ids only), >= 4, then any
+                if (cnt && TW == 16)
+                    k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, 2 * kSeenHot, set);
                 if (cnt) k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, kSeenHot, set);
                 k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, 1u, set);
             };
