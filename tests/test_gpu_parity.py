@@ -556,3 +556,21 @@ def test_sixteen_bit_static_sweep_without_waves(dev):
     lab = torch.from_numpy(oracle.random_labels(n, 11).astype(np.int32)).cuda()
     I, J = dev.gather(lab, I), dev.gather(lab, J)
     pipeline_vs_oracle(dev, I, J, n)
+
+
+@pytest.mark.parametrize("m", [0, 1, 4999, 5000])
+def test_many_vertices_few_edges(dev, m):
+    """n = 2^25 + 3 with a few thousand edges: nearly every vertex is
+    isolated, the range-pass relabel and 26-bit radix keys run on a tiny edge
+    list, and the never-seen vertices fill the tail of the order in ascending
+    id (reference _parallel.py:132-135, 197-200)."""
+    import torch
+
+    n = (1 << 25) + 3
+    rng = np.random.default_rng(m + 7)
+    I = rng.integers(0, n, m, dtype=np.int64)
+    J = rng.integers(0, n, m, dtype=np.int64)
+    if m:
+        I[0], J[-1] = n - 1, 0
+    t = lambda a: torch.from_numpy(a.astype(np.uint32).view(np.int32)).cuda()  # noqa: E731
+    pipeline_vs_oracle(dev, t(I), t(J), n)
