@@ -33,6 +33,7 @@ constexpr int kRecsPerTile = kScanNT * kRecsPerThread;
 // vertices per thread (multiple of 4; measured c4 / c5 P2: 4 -> 2.71 / 0.41 ms,
 // 8 -> 2.69 / 0.39, 16 -> 2.74 / 0.41)
 constexpr int kAssignVPT = 8;
+static_assert(kAssignVPT % 4 == 0, "labels are stored as 16-byte quads");
 constexpr int kAssignTile = kScanNT * kAssignVPT;
 
 // word w of the bitmap (position p: w = p >> 5) -> its index in the record array
@@ -351,7 +352,9 @@ __global__ void __launch_bounds__(kScanNT) k_assign_window(const uint32_t* __res
         lab[k] = r;
     }
     if (v0 + kAssignVPT <= n && (reinterpret_cast<uintptr_t>(label) & 15) == 0) {
-        *reinterpret_cast<uint4*>(label + v0) = make_uint4(lab[0], lab[1], lab[2], lab[3]);
+#pragma unroll
+        for (int q = 0; q < kAssignVPT / 4; q++)
+            reinterpret_cast<uint4*>(label + v0)[q] = make_uint4(lab[4 * q], lab[4 * q + 1], lab[4 * q + 2], lab[4 * q + 3]);
     } else {
 #pragma unroll
         for (int k = 0; k < kAssignVPT; k++)
