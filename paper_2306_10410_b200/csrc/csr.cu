@@ -287,7 +287,8 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
     if (e != cudaSuccess) return e;
     k_scan_u32<<<(unsigned)ceil_div(hcount, kScanTile), kScanTileNT, 0, s>>>(H, hcount, 0u, scan_status, counter);
     k_radix_downsweep<RB, NT, IPT, MINB, Op><<<(unsigned)tiles, NT, C::SMEM, s>>>(kin, vin, m, op, bits, tiles, H,
-                                                                                kout, vout, row_starts);
+                                                                                kout, vout, row_starts,
+                                                                                (uint32_t)(MINB * num_sms));
     return cudaGetLastError();
 }
 
