@@ -121,11 +121,10 @@ __global__ void __launch_bounds__(kFhNT, 1) k_first_hit(Ranges r, uint32_t* firs
 }
 
 // Static-mode sweep (stage 2 of the two-stage sweep): each of the two position ranges is walked
-// separately (uniform pointer and base, no per-quad range select), SeenSet
-// membership is a SWAR zero-lane test on the bucket's 64 bits, and the guard
-// load and the atomicMin are predicated instructions, not branches.
-// SeenSet membership: a SWAR zero-lane test on each of the bucket's three
-// 32-bit words (planes: word w of bucket b at set[w * kHubBuckets + b]).
+// separately (uniform pointer and base, no per-quad range select), and the
+// guard load and the atomicMin are predicated instructions, not branches.
+// SeenSet membership: a SWAR zero-lane test on each 32-bit word of the bucket
+// (planes: word w of bucket b at set[w * kHubBuckets + b]).
 template <int TW>
 __device__ __forceinline__ bool seen_swar(const uint32_t* set, const HubHash& hh, uint32_t v) {
     constexpr uint32_t kTagMask = (1u << TW) - 1u;
@@ -253,22 +252,24 @@ __global__ void k_merge_bits(uint32_t* seenb, uint32_t* newb, uint64_t words) {
 
 // SeenSet from the counting prefix: a vertex whose first occurrence is one of
 // the prefix positions (exactly one thread per vertex) and whose prefix count
-// reaches `thr` gets its tag into a free lane of its bucket.  Rounds of
-// decreasing threshold (frequent vertices first, then any) fill the lanes in
-// priority order (measured at s26: rounds 8 / 4 / 1 6.99 ms, 4 / 1 7.19,
-// 8 / 1 7.01, 2 / 1 7.80; at s22 the extra round costs more than it saves); a
-// full bucket drops the vertex: membership only ever saves work, it never
-// changes first[].  Without counts (cnt == NULL) every such vertex is offered.
+// lies in [lo, hi) gets its tag into a free lane of its bucket.  Rounds of
+// decreasing count bands (frequent vertices first, then the rest) fill the
+// lanes in priority order, each vertex offered once; a full bucket drops the
+// vertex: membership only ever saves work, it never changes first[].
+// Without counts (cnt == NULL) every such vertex is offered.
 template <int TW>
 __global__ void k_seen_build(const uint32_t* __restrict__ I, uint32_t count, uint32_t base,
                              const uint32_t* __restrict__ first, HubHash hh, const uint32_t* __restrict__ cnt,
-                             uint32_t cmask, uint32_t thr, uint32_t* set) {
+                             uint32_t cmask, uint32_t lo, uint32_t hi, uint32_t* set) {
     constexpr uint32_t kTagMask = (1u << TW) - 1u;
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= count) return;
     const uint32_t v = __ldg(I + p);
     if (__ldg(first + v) != base + p) return;   // not the first occurrence
-    if (cnt && __ldg(cnt + (hash_slot(v) & cmask)) < thr) return;
+    if (cnt) {   // this round's count band only: a vertex is offered once
+        const uint32_t c = __ldg(cnt + (hash_slot(v) & cmask));
+        if (c < lo || c >= hi) return;
+    }
     uint32_t b, tag;
     hh.split(v, b, tag);
     if (tag == kTagMask) return;                // reserved for "empty"
@@ -427,11 +428,17 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
             }
             auto build = [&](auto tw) {
                 constexpr int TW = decltype(tw)::value;
-                // fill rounds, most frequent first: counts >= 8 (wide ids only), >= 4, then any
+                // fill rounds, most frequent first: counts >= 8 (wide ids only), [4, 8), then the rest
+                constexpr uint32_t kAll = 0xFFFFFFFFu;
+                const uint32_t hot_hi = TW == 16 ? 2 * kSeenHot : kAll;
                 if (cnt && TW == 16)
-                    k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, 2 * kSeenHot, set);
-                if (cnt) k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, kSeenHot, set);
-                k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, 1u, set);
+                    k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, 2 * kSeenHot, kAll,
+                                                        set);
+                if (cnt)
+                    k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, kSeenHot, hot_hi,
+                                                        set);
+                k_seen_build<TW><<<pg, 256, 0, s>>>(I, prefix, base_i, first, hh, cnt, cmask, 1u,
+                                                    cnt ? kSeenHot : kAll, set);
             };
             Ranges r2{I + prefix, quads - qp, base_i + prefix, J, quads, base_j};
             // first[] beyond L2 (n > 2^23, > 32 MB): guard on a seen-bitmap in geometric waves
