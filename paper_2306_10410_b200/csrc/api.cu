@@ -106,6 +106,7 @@ bool spmv_partition_ok(const void* ws, const SpmvKey& k, bool reuse) {
 struct boba_graph {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    uint64_t body_kernels = 0;  // kernels inside the taken branch of conditional nodes
 };
 
 // Host-buffer contexts: two buffer slots so that consecutive graphs overlap
@@ -331,7 +332,8 @@ int boba_reorder_to_csr_timed(const uint32_t* I, const uint32_t* J, const double
     cudaError_t e = boba::launch_first_hit_shard(I, J, m, m, 0, n, first, false, hubs, sms, s, bits_ws);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: first occurrence");
     mark(1);
-    e = boba::launch_compact(first, m, n, order, label, nullptr, hubs, rest, rest_bytes, sms, s);
+    // counts[0]: the number of vertices first seen in I, which bounds every CSR row
+    e = boba::launch_compact(first, m, n, order, label, nullptr, hubs, rest, rest_bytes, sms, s, counts);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: compact");
     mark(2);
     // the relabel may also count the first radix digit of its rows (the
@@ -340,8 +342,8 @@ int boba_reorder_to_csr_timed(const uint32_t* I, const uint32_t* J, const double
     e = boba::launch_relabel(I, J, m, label, hubs, I2, J2, nullptr, n, sms, s, &rh);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: relabel");
     mark(3);
-    e = boba::launch_coo_to_csr(I2, J2, w, m, n, nullptr, offsets, indices, w_out, rest, rest_bytes, sms, s, rh.done);
-    (void)counts;
+    e = boba::launch_coo_to_csr(I2, J2, w, m, n, nullptr, offsets, indices, w_out, rest, rest_bytes, sms, s, rh.done,
+                                counts);
     if (e != cudaSuccess) return cuda_status(e, "boba_reorder_to_csr: coo_to_csr");
     mark(4);
     return BOBA_OK;
@@ -374,8 +376,10 @@ int boba_reorder_to_csr_graph_create(const uint32_t* I, const uint32_t* J, uint6
     boba_graph* g = new boba_graph();
     if (rc == BOBA_OK && e == cudaSuccess) e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
     if (rc == BOBA_OK && e == cudaSuccess) {
+        boba::take_conditional_body_kernels();
         rc = boba_reorder_to_csr(I, J, nullptr, m, n, first, order, label, I2, J2, offsets, indices, nullptr, ws,
                                  ws_bytes, st);
+        g->body_kernels = boba::take_conditional_body_kernels();
         cudaError_t e2 = cudaStreamEndCapture(st, &g->graph);
         if (e == cudaSuccess) e = e2;
     }
@@ -401,14 +405,16 @@ int boba_graph_kernel_nodes(const boba_graph* g, uint64_t* count) {
     if (e != cudaSuccess) return cuda_status(e, "boba_graph_kernel_nodes");
     std::vector<cudaGraphNode_t> nodes(num);
     if (num) e = cudaGraphGetNodes(g->graph, nodes.data(), &num);
-    uint64_t k = 0;
-    for (size_t i = 0; e == cudaSuccess && i < num; i++) {
-        cudaGraphNodeType t;
-        e = cudaGraphNodeGetType(nodes[i], &t);
-        k += e == cudaSuccess && t == cudaGraphNodeTypeKernel;
-    }
     if (e != cudaSuccess) return cuda_status(e, "boba_graph_kernel_nodes");
-    *count = k;
+    uint64_t k = 0;
+    for (size_t i = 0; i < num; i++) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess)
+            k += t == cudaGraphNodeTypeKernel;
+        else
+            cudaGetLastError();  // a node type this query does not know (conditional): counted below
+    }
+    *count = k + g->body_kernels;
     return BOBA_OK;
 }
 

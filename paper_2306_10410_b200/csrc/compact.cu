@@ -207,9 +207,16 @@ CompactWs carve_compact(void* base, uint64_t m, uint32_t n) {
 
 size_t compact_workspace_bytes(uint64_t m, uint32_t n) { return carve_compact(nullptr, m, n).total; }
 
+// Vertices whose first occurrence lies in I = set bits of the map before
+// position m.  Every CSR row is the label of such a vertex (it occurs in I),
+// so this bounds the rows COO->CSR has to sort.
+__global__ void k_seen_in_first_half(const uint4* __restrict__ recs, uint64_t m, uint32_t* out) {
+    *out = m ? rank_of((uint32_t)m, recs) : 0u;
+}
+
 cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order,
                            uint32_t* label, uint32_t* n_seen_out, unsigned long long* hubs, void* ws,
-                           size_t ws_bytes, int num_sms, cudaStream_t s) {
+                           size_t ws_bytes, int num_sms, cudaStream_t s, uint32_t* rows_bound_out) {
     if (ws_bytes < compact_workspace_bytes(m, n)) return cudaErrorInvalidValue;
     if (n == 0) return cudaSuccess;
     const uint64_t nrec = num_recs(m);
@@ -231,6 +238,8 @@ cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32
     k_assign<<<(int)v_tiles, kScanNT, 0, s>>>(first, n, reinterpret_cast<const uint4*>(w.recs), n_seen, order, label,
                                               w.st_v, counters + 1);
     if (n_seen_out) cudaMemcpyAsync(n_seen_out, n_seen, 4, cudaMemcpyDeviceToDevice, s);
+    if (rows_bound_out)
+        k_seen_in_first_half<<<1, 1, 0, s>>>(reinterpret_cast<const uint4*>(w.recs), m, rows_bound_out);
     if (hubs) {
         // HubLabels (hubs.cuh) for phase 3: labels [0, kHubMaxLabel), kHubWays
         // slots per bucket, the smallest labels of each bucket (one pass).

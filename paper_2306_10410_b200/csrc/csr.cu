@@ -72,6 +72,12 @@ __global__ void __launch_bounds__(kOffNT) k_scan_offsets(const uint32_t* __restr
 
 __global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
 
+// zeroes words[0, n) and *also (kernel-node replacement for two memsets)
+__global__ void k_zero_u32(uint32_t* words, uint64_t n, uint32_t* also) {
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) words[i] = 0u;
+    if (threadIdx.x == 0) *also = 0u;
+}
+
 static cudaError_t launch_set_u32(uint32_t* p, uint32_t v, cudaStream_t s) {
     k_set_u32<<<1, 1, 0, s>>>(p, v);
     return cudaGetLastError();
@@ -220,10 +226,11 @@ struct CsrPlan {
     uint64_t tile = 0;
 };
 
-CsrPlan plan_for(uint32_t n) {
+int key_bits(uint32_t n) { return n <= 1 ? 0 : 32 - __builtin_clz(n - 1); }
+
+CsrPlan plan_bits(int kbits) {
     CsrPlan p;
-    const int kbits = n <= 1 ? 0 : 32 - __builtin_clz(n - 1);
-    if (kbits == 0) return p;
+    if (kbits <= 0) return p;
     p.passes = (kbits + kRadixBits - 1) / kRadixBits;
     int sh = 0;
     for (int i = 0; i < p.passes; i++) {
@@ -235,6 +242,8 @@ CsrPlan plan_for(uint32_t n) {
     p.tile = kRadixTile;
     return p;
 }
+
+CsrPlan plan_for(uint32_t n) { return plan_bits(key_bits(n)); }
 
 struct CsrWs {
     uint32_t* counts;
@@ -272,7 +281,8 @@ CsrWs carve(void* base, uint64_t m, uint32_t n) {
 template <int RB, int NT, int IPT, int MINB, typename Op = DigitShift>
 cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, Op op, int bits, uint32_t* H,
                           unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                          int num_sms, cudaStream_t s, uint32_t* row_starts = nullptr, bool h_ready = false) {
+                          int num_sms, cudaStream_t s, uint32_t* row_starts = nullptr, bool h_ready = false,
+                          bool zero_by_kernel = false) {
     using C = RadixCfg<RB, NT, IPT>;
     static PerDeviceOnce attr;
     if (cudaError_t e = set_attr_once(attr, k_radix_downsweep<RB, NT, IPT, MINB, Op>,
@@ -282,8 +292,14 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
     const uint64_t hcount = tiles << bits;
     const uint64_t up_grid = tiles < (uint64_t)num_sms * 8 ? tiles : (uint64_t)num_sms * 8;
     if (!h_ready) k_radix_upsweep<RB, NT, IPT, Op><<<(unsigned)up_grid, NT, 0, s>>>(kin, m, op, bits, tiles, H);
-    cudaError_t e = cudaMemsetAsync(scan_status, 0, (ceil_div(hcount, kScanTile) + 1) * 8, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 4, s);
+    cudaError_t e = cudaSuccess;
+    if (zero_by_kernel) {   // inside a conditional graph body: kernel nodes only
+        k_zero_u32<<<1, 256, 0, s>>>(reinterpret_cast<uint32_t*>(scan_status), (ceil_div(hcount, kScanTile) + 1) * 2,
+                                     counter);
+    } else {
+        e = cudaMemsetAsync(scan_status, 0, (ceil_div(hcount, kScanTile) + 1) * 8, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 4, s);
+    }
     if (e != cudaSuccess) return e;
     k_scan_u32<<<(unsigned)ceil_div(hcount, kScanTile), kScanTileNT, 0, s>>>(H, hcount, 0u, scan_status, counter);
     k_radix_downsweep<RB, NT, IPT, MINB, Op><<<(unsigned)tiles, NT, C::SMEM, s>>>(kin, vin, m, op, bits, tiles, H,
@@ -297,21 +313,39 @@ cudaError_t radix_pass_op(const uint32_t* kin, const uint32_t* vin, uint64_t m, 
 template <int RB, int NT, int IPT, int MINB>
 cudaError_t radix_pass(const uint32_t* kin, const uint32_t* vin, uint64_t m, int shift, int bits, uint32_t* H,
                        unsigned long long* scan_status, unsigned* counter, uint32_t* kout, uint32_t* vout,
-                       int num_sms, cudaStream_t s, uint32_t* row_starts, bool h_ready = false) {
+                       int num_sms, cudaStream_t s, uint32_t* row_starts, bool h_ready = false,
+                       bool zero_by_kernel = false) {
     const DigitShift op{shift, (1u << bits) - 1u};
     if (RB == 8 && bits <= 6)
         return radix_pass_op<6, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                           num_sms, s, row_starts, h_ready);
+                                                           num_sms, s, row_starts, h_ready, zero_by_kernel);
     if (RB == 8 && bits == 7)
         return radix_pass_op<7, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                           num_sms, s, row_starts, h_ready);
+                                                           num_sms, s, row_starts, h_ready, zero_by_kernel);
     return radix_pass_op<RB, NT, IPT, MINB, DigitShift>(kin, vin, m, op, bits, H, scan_status, counter, kout, vout,
-                                                        num_sms, s, row_starts, h_ready);
+                                                        num_sms, s, row_starts, h_ready, zero_by_kernel);
+}
+
+// Kernels captured into the IF body of the last conditional node built on this
+// thread (both bodies launch the same number): the captured graph's kernel
+// count, which cannot be read back from a conditional node.
+thread_local uint64_t t_cond_body_kernels = 0;
+
+// Conditional-graph plan choice: 1 = every row is below 2^(kbits-1), the
+// plan with a key bit less is exact (body 0), else the full-width plan.
+__global__ void k_plan_cond(const uint32_t* __restrict__ rows_bound, uint32_t half, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, *rows_bound <= half ? 1u : 0u);
 }
 
 }  // namespace
 
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool /*weighted*/) { return carve(nullptr, m, n).total; }
+
+uint64_t take_conditional_body_kernels() {
+    const uint64_t k = t_cond_body_kernels;
+    t_cond_body_kernels = 0;
+    return k;
+}
 
 // The first radix pass's tile histogram alone (its upsweep), into the
 // workspace launch_coo_to_csr(..., first_hist_ready = true) reads it from: a
@@ -484,7 +518,8 @@ cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* cou
 
 cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
                               const uint32_t* counts_in, uint32_t* offsets, uint32_t* indices, double* w_out,
-                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool first_hist_ready) {
+                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool first_hist_ready,
+                              const uint32_t* rows_bound) {
     const bool weighted = w != nullptr;
     CsrWs W = carve(ws, m, n);
     if (ws_bytes < W.total) return cudaErrorInvalidValue;
@@ -516,16 +551,81 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
         if (e == cudaSuccess) e = launch_set_u32(offsets + n, (uint32_t)m, s);
         if (e != cudaSuccess) return e;
     }
-    for (int i = 0; i < p.passes; i++) {
-        const bool last = i == p.passes - 1;
-        // pass i writes bufs[2(i&1)], bufs[2(i&1)+1]; it reads the other parity.
-        uint32_t* kout = last ? nullptr : W.bufs[(i & 1) * 2];
-        uint32_t* vout = (last && !weighted) ? indices : W.bufs[(i & 1) * 2 + 1];
-        e = radix_pass<8, 256, 16, 4>(kin, vin, m, p.shift[i], p.bits[i], W.H, W.scan_status, W.counters, kout, vout,
-                                      num_sms, s, (last && !counts_in) ? offsets : nullptr, i == 0 && first_hist_ready);
+    // Under CUDA-graph capture with a device-side row bound: after the first
+    // pass, an IF/ELSE conditional node runs either the plan with a key bit
+    // less (rows below 2^(kbits-1), decided on the device per replay) or the
+    // full-width one; both share that first pass.  Elsewhere: the full plan.
+    CsrPlan pa;
+    bool cond = false;
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (rows_bound && !counts_in && p.passes >= 2 && cudaStreamIsCapturing(s, &cst) == cudaSuccess &&
+        cst == cudaStreamCaptureStatusActive) {
+        pa = plan_bits(key_bits(n) - 1);
+        cond = pa.passes == p.passes && pa.bits[0] == p.bits[0];
+    }
+    auto run_passes = [&](const CsrPlan& q, int from, int to, const uint32_t* k0, const uint32_t* v0,
+                          cudaStream_t st, bool in_body) -> cudaError_t {
+        const uint32_t* ki = k0;
+        const uint32_t* vi = v0;
+        for (int i = from; i < to; i++) {
+            const bool last = i == q.passes - 1;
+            // pass i writes bufs[2(i&1)], bufs[2(i&1)+1]; it reads the other parity.
+            uint32_t* kout = last ? nullptr : W.bufs[(i & 1) * 2];
+            uint32_t* vout = (last && !weighted) ? indices : W.bufs[(i & 1) * 2 + 1];
+            cudaError_t r = radix_pass<8, 256, 16, 4>(ki, vi, m, q.shift[i], q.bits[i], W.H, W.scan_status,
+                                                      W.counters, kout, vout, num_sms, st,
+                                                      (last && !counts_in) ? offsets : nullptr,
+                                                      i == 0 && first_hist_ready, in_body);
+            if (r != cudaSuccess) return r;
+            ki = kout;
+            vi = vout;
+        }
+        kin = ki;
+        vin = vi;
+        return cudaSuccess;
+    };
+    if (!cond) {
+        e = run_passes(p, 0, p.passes, kin, vin, s, false);
         if (e != cudaSuccess) return e;
-        kin = kout;
-        vin = vout;
+    } else {
+        e = run_passes(p, 0, 1, kin, vin, s, false);   // the shared first pass
+        if (e != cudaSuccess) return e;
+        const uint32_t* k1 = W.bufs[0];
+        const uint32_t* v1 = W.bufs[1];
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        cudaGraphConditionalHandle h;
+        e = cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &nd);
+        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, g, 0, 0);
+        if (e != cudaSuccess) return e;
+        k_plan_cond<<<1, 1, 0, s>>>(rows_bound, 1u << (key_bits(n) - 1), h);
+        e = cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &nd);
+        if (e != cudaSuccess) return e;
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 2;
+        cudaGraphNode_t cn;
+        e = cudaGraphAddNode(&cn, g, deps, nd, &cp);
+        if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(s, &cn, 1, cudaStreamSetCaptureDependencies);
+        if (e != cudaSuccess) return e;
+        for (int body = 0; body < 2; body++) {
+            cudaStream_t bs = nullptr;
+            e = cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking);
+            if (e != cudaSuccess) return e;
+            e = cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[body], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeRelaxed);
+            const CsrPlan& q = body == 0 ? pa : p;
+            if (body == 0) t_cond_body_kernels += 4ull * (q.passes - 1);   // zero, upsweep, scan, downsweep
+            cudaError_t e2 = e == cudaSuccess ? run_passes(q, 1, q.passes, k1, v1, bs, true) : e;
+            cudaGraph_t done = nullptr;
+            if (e == cudaSuccess) e = cudaStreamEndCapture(bs, &done);
+            cudaStreamDestroy(bs);
+            if (e2 != cudaSuccess) return e2;
+            if (e != cudaSuccess) return e;
+        }
     }
     if (!counts_in) {
         const uint64_t sm_tiles = ceil_div((uint64_t)n + 1, kSmTile);

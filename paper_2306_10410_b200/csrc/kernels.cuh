@@ -21,9 +21,11 @@ cudaError_t launch_first_hit_shard(const uint32_t* I, const uint32_t* J, uint64_
 
 size_t compact_workspace_bytes(uint64_t m, uint32_t n);
 // hubs (may be NULL): kHubTableBytes table filled for phase 3 (hubs.cuh)
+// rows_bound_out (device word, may be NULL): the number of vertices first seen
+// in I -- every relabelled source row is below it
 cudaError_t launch_compact(const uint32_t* first, uint64_t m, uint32_t n, uint32_t* order, uint32_t* label,
                            uint32_t* n_seen_out, unsigned long long* hubs, void* ws, size_t ws_bytes, int num_sms,
-                           cudaStream_t s);
+                           cudaStream_t s, uint32_t* rows_bound_out = nullptr);
 
 // The first radix pass of COO->CSR needs the digit histogram of every
 // 4096-row tile of I2; the relabel that writes I2 can produce it on the way
@@ -48,11 +50,15 @@ cudaError_t launch_hist(const uint32_t* I, uint64_t m, uint32_t n, uint32_t* cou
 cudaError_t launch_row_offsets(const uint32_t* counts, uint32_t n, uint32_t* offsets, unsigned long long* status,
                                unsigned* counter, cudaStream_t s);
 size_t coo_to_csr_workspace_bytes(uint64_t m, uint32_t n, bool weighted);
+// kernels a graph capture on this thread put inside conditional-node bodies
+// (the taken branch's count), reset by the call
+uint64_t take_conditional_body_kernels();
 // first_hist_ready: the relabel already wrote the first pass's tile histogram
 // (coo_to_csr_first_hist of the same workspace)
 cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const double* w, uint64_t m, uint32_t n,
                               const uint32_t* counts_in, uint32_t* offsets, uint32_t* indices, double* w_out,
-                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool first_hist_ready = false);
+                              void* ws, size_t ws_bytes, int num_sms, cudaStream_t s, bool first_hist_ready = false,
+                              const uint32_t* rows_bound = nullptr);
 
 size_t spmv_workspace_bytes(uint32_t n, uint64_t m);
 cudaError_t launch_spmv(const uint32_t* offsets, const uint32_t* indices, const float* w, const float* x, float* y,

@@ -574,3 +574,36 @@ def test_many_vertices_few_edges(dev, m):
         I[0], J[-1] = n - 1, 0
     t = lambda a: torch.from_numpy(a.astype(np.uint32).view(np.int32)).cuda()  # noqa: E731
     pipeline_vs_oracle(dev, t(I), t(J), n)
+
+
+def test_captured_pipeline_picks_the_radix_plan_per_replay(dev):
+    """The captured step carries both COO->CSR pass plans behind a conditional
+    node: the one with a key bit less when every source row is below
+    2^(kbits-1) (decided on the device from the count of vertices first seen
+    in I), the full-width one otherwise.  Replays that need each plan, in both
+    orders, against the oracle (reference graph.py:253-277)."""
+    import torch
+
+    n, m = 1 << 18, 1 << 20
+    rng = np.random.default_rng(23)
+
+    def edges(sources):   # the first-seen-in-I count is about `sources`
+        I = rng.integers(0, n, sources)[rng.integers(0, sources, m)]
+        J = rng.integers(0, n, m)
+        return (torch.from_numpy(I.astype(np.uint32).view(np.int32)).cuda(),
+                torch.from_numpy(J.astype(np.uint32).view(np.int32)).cuda())
+
+    narrow, wide = edges(60000), edges(200000)   # rows < 2^17, rows beyond 2^17
+    I, J = narrow[0].clone(), narrow[1].clone()
+    pipe = dev.Pipeline(m, n)
+    g = dev.CapturedPipeline(pipe, I, J)
+    u = lambda t: t.cpu().numpy().view(np.uint32).astype(np.int64)  # noqa: E731
+    for I_new, J_new in (wide, narrow, wide):
+        I.copy_(I_new)
+        J.copy_(J_new)
+        g.launch()
+        torch.cuda.synchronize()
+        order, label, I2, J2, off, idx, _ = oracle.pipeline(u(I_new), u(J_new), n)
+        assert np.array_equal(u(pipe.order[:n]), order) and np.array_equal(u(pipe.label[:n]), label)
+        assert np.array_equal(u(pipe.offsets[: n + 1]), off) and np.array_equal(u(pipe.indices[:m]), idx)
+    g.close()
