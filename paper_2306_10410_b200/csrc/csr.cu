@@ -561,7 +561,9 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
     if (rows_bound && !counts_in && p.passes >= 2 && cudaStreamIsCapturing(s, &cst) == cudaSuccess &&
         cst == cudaStreamCaptureStatusActive) {
         pa = plan_bits(key_bits(n) - 1);
-        cond = pa.passes == p.passes && pa.bits[0] == p.bits[0];
+        // the plans share their first pass when its digit is the same; else both
+        // run whole inside the branches (not with a first histogram made for p)
+        cond = pa.passes == p.passes && (pa.bits[0] == p.bits[0] || !first_hist_ready);
     }
     auto run_passes = [&](const CsrPlan& q, int from, int to, const uint32_t* k0, const uint32_t* v0,
                           cudaStream_t st, bool in_body) -> cudaError_t {
@@ -588,10 +590,13 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
         e = run_passes(p, 0, p.passes, kin, vin, s, false);
         if (e != cudaSuccess) return e;
     } else {
-        e = run_passes(p, 0, 1, kin, vin, s, false);   // the shared first pass
-        if (e != cudaSuccess) return e;
-        const uint32_t* k1 = W.bufs[0];
-        const uint32_t* v1 = W.bufs[1];
+        const int from = pa.bits[0] == p.bits[0] ? 1 : 0;
+        if (from) {
+            e = run_passes(p, 0, 1, kin, vin, s, false);   // the shared first pass
+            if (e != cudaSuccess) return e;
+        }
+        const uint32_t* k1 = from ? W.bufs[0] : kin;
+        const uint32_t* v1 = from ? W.bufs[1] : vin;
         cudaGraph_t g = nullptr;
         const cudaGraphNode_t* deps = nullptr;
         size_t nd = 0;
@@ -618,8 +623,8 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
             e = cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[body], nullptr, nullptr, 0,
                                               cudaStreamCaptureModeRelaxed);
             const CsrPlan& q = body == 0 ? pa : p;
-            if (body == 0) t_cond_body_kernels += 4ull * (q.passes - 1);   // zero, upsweep, scan, downsweep
-            cudaError_t e2 = e == cudaSuccess ? run_passes(q, 1, q.passes, k1, v1, bs, true) : e;
+            if (body == 0) t_cond_body_kernels += 4ull * (q.passes - from);   // zero, upsweep, scan, downsweep
+            cudaError_t e2 = e == cudaSuccess ? run_passes(q, from, q.passes, k1, v1, bs, true) : e;
             cudaGraph_t done = nullptr;
             if (e == cudaSuccess) e = cudaStreamEndCapture(bs, &done);
             cudaStreamDestroy(bs);

@@ -576,15 +576,18 @@ def test_many_vertices_few_edges(dev, m):
     pipeline_vs_oracle(dev, t(I), t(J), n)
 
 
-def test_captured_pipeline_picks_the_radix_plan_per_replay(dev):
+@pytest.mark.parametrize("logn", [18, 22])
+def test_captured_pipeline_picks_the_radix_plan_per_replay(dev, logn):
     """The captured step carries both COO->CSR pass plans behind a conditional
     node: the one with a key bit less when every source row is below
     2^(kbits-1) (decided on the device from the count of vertices first seen
     in I), the full-width one otherwise.  Replays that need each plan, in both
-    orders, against the oracle (reference graph.py:253-277)."""
+    orders, against the oracle (reference graph.py:253-277).  At n = 2^18 the
+    two plans share their first pass (6/6/6 vs 6/6/5 bits); at 2^22 they do
+    not (8/7/7 vs 7/7/7) and the whole sort sits in the branches."""
     import torch
 
-    n, m = 1 << 18, 1 << 20
+    n, m = 1 << logn, 1 << 20
     rng = np.random.default_rng(23)
 
     def edges(sources):   # the first-seen-in-I count is about `sources`
@@ -593,7 +596,7 @@ def test_captured_pipeline_picks_the_radix_plan_per_replay(dev):
         return (torch.from_numpy(I.astype(np.uint32).view(np.int32)).cuda(),
                 torch.from_numpy(J.astype(np.uint32).view(np.int32)).cuda())
 
-    narrow, wide = edges(60000), edges(200000)   # rows < 2^17, rows beyond 2^17
+    narrow, wide = edges(n // 4), edges(3 * n // 4)   # rows < n/2 (a key bit less), rows beyond it
     I, J = narrow[0].clone(), narrow[1].clone()
     pipe = dev.Pipeline(m, n)
     g = dev.CapturedPipeline(pipe, I, J)
