@@ -185,6 +185,13 @@ int boba_reorder_to_csr_graph_create(const uint32_t *I, const uint32_t *J, uint6
                                      uint32_t *first, uint32_t *order, uint32_t *label, uint32_t *I2,
                                      uint32_t *J2, uint32_t *offsets, uint32_t *indices, void *workspace,
                                      size_t workspace_bytes, boba_graph **out);
+/* The same graph with event-record nodes at the phase boundaries (events as
+ * in boba_reorder_to_csr_timed; each replay records them), for per-phase
+ * times of exactly the replayed step. */
+int boba_reorder_to_csr_graph_create_timed(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n,
+                                           uint32_t *first, uint32_t *order, uint32_t *label, uint32_t *I2,
+                                           uint32_t *J2, uint32_t *offsets, uint32_t *indices, void *workspace,
+                                           size_t workspace_bytes, void *const *events, boba_graph **out);
 int boba_graph_launch(boba_graph *graph, void *stream);
 void boba_reorder_to_csr_graph_destroy(boba_graph *graph);
 /* Number of kernel launches one boba_graph_launch replays (the graph's

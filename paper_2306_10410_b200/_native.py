@@ -83,6 +83,8 @@ SIGNATURES = {
                                           _P, _P, _SZ, _P], _I),
     "boba_reorder_to_csr_graph_create": ([_P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ,
                                           ctypes.POINTER(_P)], _I),
+    "boba_reorder_to_csr_graph_create_timed": ([_P, _P, _U64, _U32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P,
+                                                ctypes.POINTER(_P)], _I),
     "boba_graph_launch": ([_P, _P], _I),
     "boba_reorder_to_csr_graph_destroy": ([_P], None),
     "boba_graph_kernel_nodes": ([_P, _P], _I),

@@ -314,8 +314,15 @@ int boba_reorder_to_csr_timed(const uint32_t* I, const uint32_t* J, const double
     REQUIRE(!w || w_out || m == 0, "boba_reorder_to_csr: weights given but weights_out is NULL");
     if (n == 0) return BOBA_OK;
     cudaStream_t s = S(stream);
+    // under stream capture a plain record would only order the capture:
+    // record external events so each graph replay records them
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    const bool capturing = events && cudaStreamIsCapturing(s, &cst) == cudaSuccess &&
+                           cst == cudaStreamCaptureStatusActive;
     auto mark = [&](int i) {
-        if (events && events[i]) cudaEventRecord(static_cast<cudaEvent_t>(events[i]), s);
+        if (events && events[i])
+            cudaEventRecordWithFlags(static_cast<cudaEvent_t>(events[i]), s,
+                                     capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     };
     char* base = static_cast<char*>(ws);
     uint32_t* counts = reinterpret_cast<uint32_t*>(base);
@@ -357,9 +364,10 @@ int boba_reorder_to_csr(const uint32_t* I, const uint32_t* J, const double* w, u
                                      ws_bytes, stream, nullptr);
 }
 
-int boba_reorder_to_csr_graph_create(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
-                                     uint32_t* order, uint32_t* label, uint32_t* I2, uint32_t* J2, uint32_t* offsets,
-                                     uint32_t* indices, void* ws, size_t ws_bytes, boba_graph** out) {
+int boba_reorder_to_csr_graph_create_timed(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n,
+                                           uint32_t* first, uint32_t* order, uint32_t* label, uint32_t* I2,
+                                           uint32_t* J2, uint32_t* offsets, uint32_t* indices, void* ws,
+                                           size_t ws_bytes, void* const* events, boba_graph** out) {
     REQUIRE(out, "boba_reorder_to_csr_graph_create: out is NULL");
     REQUIRE(n >= 2, "boba_reorder_to_csr_graph_create: n must be >= 2 (use boba_reorder_to_csr)");
     // the inputs may still be in flight on any of the caller's streams: the
@@ -377,8 +385,8 @@ int boba_reorder_to_csr_graph_create(const uint32_t* I, const uint32_t* J, uint6
     if (rc == BOBA_OK && e == cudaSuccess) e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
     if (rc == BOBA_OK && e == cudaSuccess) {
         boba::take_conditional_body_kernels();
-        rc = boba_reorder_to_csr(I, J, nullptr, m, n, first, order, label, I2, J2, offsets, indices, nullptr, ws,
-                                 ws_bytes, st);
+        rc = boba_reorder_to_csr_timed(I, J, nullptr, m, n, first, order, label, I2, J2, offsets, indices, nullptr, ws,
+                                       ws_bytes, st, events);
         g->body_kernels = boba::take_conditional_body_kernels();
         cudaError_t e2 = cudaStreamEndCapture(st, &g->graph);
         if (e == cudaSuccess) e = e2;
@@ -391,6 +399,13 @@ int boba_reorder_to_csr_graph_create(const uint32_t* I, const uint32_t* J, uint6
     }
     *out = g;
     return BOBA_OK;
+}
+
+int boba_reorder_to_csr_graph_create(const uint32_t* I, const uint32_t* J, uint64_t m, uint32_t n, uint32_t* first,
+                                     uint32_t* order, uint32_t* label, uint32_t* I2, uint32_t* J2, uint32_t* offsets,
+                                     uint32_t* indices, void* ws, size_t ws_bytes, boba_graph** out) {
+    return boba_reorder_to_csr_graph_create_timed(I, J, m, n, first, order, label, I2, J2, offsets, indices, ws,
+                                                  ws_bytes, nullptr, out);
 }
 
 int boba_graph_launch(boba_graph* g, void* stream) {

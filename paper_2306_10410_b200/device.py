@@ -235,13 +235,19 @@ class CapturedPipeline:
     graph (boba_reorder_to_csr_graph_create); launch() replays the whole
     step with one graph launch.  Creating it runs the pipeline once."""
 
-    def __init__(self, pipe: "Pipeline", I: torch.Tensor, J: torch.Tensor):
+    def __init__(self, pipe: "Pipeline", I: torch.Tensor, J: torch.Tensor, events=None):
+        """events: 5 CUDA event handles recorded at the phase boundaries of
+        every replay (boba_reorder_to_csr_graph_create_timed), or None."""
         self.pipe, self.I, self.J = pipe, I, J  # keep the buffers alive
         self._g = ctypes.c_void_p()
         p = pipe
-        N.check(N.lib.boba_reorder_to_csr_graph_create(
-            _p(I), _p(J), I.numel(), p.n, _p(p.first), _p(p.order), _p(p.label), _p(p.I2), _p(p.J2), _p(p.offsets),
-            _p(p.indices), _p(p.ws), p.ws.numel(), ctypes.byref(self._g)))
+        args = (_p(I), _p(J), I.numel(), p.n, _p(p.first), _p(p.order), _p(p.label), _p(p.I2), _p(p.J2),
+                _p(p.offsets), _p(p.indices), _p(p.ws), p.ws.numel())
+        if events is None:
+            N.check(N.lib.boba_reorder_to_csr_graph_create(*args, ctypes.byref(self._g)))
+        else:
+            self._events = events
+            N.check(N.lib.boba_reorder_to_csr_graph_create_timed(*args, events, ctypes.byref(self._g)))
 
     def launch(self):
         N.check(N.lib.boba_graph_launch(self._g, _s()))
