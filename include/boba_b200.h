@@ -179,7 +179,10 @@ int boba_reorder_to_csr_timed(const uint32_t *I, const uint32_t *J, const double
  * buffers must stay allocated and the input contents may change between
  * launches; (m, n) are fixed.  n >= 2.  Creation synchronises the device
  * first (the eager run uses a private stream, so pending writes of I and J
- * on any caller stream must have landed). */
+ * on any caller stream must have landed).  In the captured step COO->CSR
+ * chooses its radix plan on the device at every replay (a conditional graph
+ * node): one key bit fewer when the relabelled rows allow it, the
+ * full-width plan otherwise -- the outputs are the same either way. */
 typedef struct boba_graph boba_graph;
 int boba_reorder_to_csr_graph_create(const uint32_t *I, const uint32_t *J, uint64_t m, uint32_t n,
                                      uint32_t *first, uint32_t *order, uint32_t *label, uint32_t *I2,
