@@ -7,7 +7,8 @@ row cut, relative range partition) and the host transfers.  Argument
 "waves": instead, one pipeline at n = 2^25 (wave-guarded first occurrence,
 range-pass relabel with the fused first radix histogram).  The default run
 also takes one s17 graph through the two-stage first occurrence (counting
-prefix, frequency-ordered SeenSet fill)."""
+prefix, frequency-ordered SeenSet fill) and replays a captured step through
+both branches of COO->CSR's conditional radix plan."""
 import os
 import sys
 
@@ -34,6 +35,26 @@ if len(sys.argv) > 1 and sys.argv[1] == "waves":
 # two-stage first occurrence with the counting prefix (m >= 16 x 64K)
 I, J = D.generate_rmat(17, 16, 2)
 D.Pipeline(I.numel(), 1 << 17).run(I, J)
+# the captured step: COO->CSR's conditional radix plan (n = 2^18: both plans share the first pass),
+# replayed once on the narrow and once on the wide branch
+n18 = 1 << 18
+rng = np.random.default_rng(5)
+def _edges(src):
+    a = rng.integers(0, n18, src)[rng.integers(0, src, 1 << 20)]
+    b = rng.integers(0, n18, 1 << 20)
+    return (torch.from_numpy(a.astype(np.uint32).view(np.int32)).cuda(),
+            torch.from_numpy(b.astype(np.uint32).view(np.int32)).cuda())
+In, Jn = _edges(n18 // 4) if not os.environ.get("SKIP_GRAPH") else (None, None)
+if In is not None:
+    Iw, Jw = _edges(3 * n18 // 4)
+    cp = D.Pipeline(1 << 20, n18)
+    g = D.CapturedPipeline(cp, In, Jn)
+    g.launch()
+    In.copy_(Iw)
+    Jn.copy_(Jw)
+    g.launch()
+    torch.cuda.synchronize()
+    g.close()
 scale = 14
 n = 1 << scale
 I, J = D.generate_rmat(scale, 8, 1)
