@@ -32,6 +32,20 @@ namespace boba {
 // CTAs lose less to the two block barriers of this latency-bound tile.
 constexpr int kSpNT = 128, kSpIPT = 8, kSpTile = kSpNT * kSpIPT;
 constexpr int kSpShort = 8;  // longest in-tile row the per-row fold takes (longer: divergent folds)
+// Whole-matrix row mode: when no row is longer than kSpRowMax (a mesh / road
+// graph), k_spmv_merge skips the merge-path tiling and gives every row one
+// thread that sums it sequentially straight from global memory -- no staging,
+// no barriers, no carries (profiles/r02_spmv_rowmap.log: on the c3 grid a
+// thread per row beats 4/8/16/32 lanes per row and the merge path; on R-MAT
+// it is 20x slower).  The longest row is found on the device when the CSR is
+// partitioned and the mode travels in the tile coordinates, so one kernel
+// serves both modes with no host round trip.  Measured, fp32 per call, c3:
+// BOBA order 0.191 -> 0.155 ms, random order 0.361 -> 0.380; R-MAT c2/c5/c4
+// unchanged (profiles/r02_spmv_rowmode.log).  Kept at 32 registers: a second
+// row per thread (c3 BOBA 0.126 ms) or a separate row kernel beside an idle
+// merge launch (0.175) cost the R-MAT path 3-10 %.
+constexpr uint32_t kSpRowMax = 8;
+constexpr uint32_t kSpRowMode = 0x80000000u;  // flag bit in coords[]
 
 // Streaming loads that must not evict the x vector's hot lines from L1.
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
@@ -74,16 +88,68 @@ __device__ __forceinline__ uint64_t merge_search(const uint32_t* a, uint64_t a_l
     return lo;
 }
 
+// Longest row of the CSR (rowmax zeroed beforehand); k_spmv_partition then
+// marks row mode in bit 31 of every tile coordinate (row ids < 2^31), so the
+// tiles learn the mode from the load they make anyway.
+__global__ void k_spmv_rowmax(const uint32_t* __restrict__ offsets, uint32_t n, uint32_t* rowmax) {
+    uint32_t mx = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t len = __ldg(offsets + i + 1) - __ldg(offsets + i);
+        mx = len > mx ? len : mx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t v = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+        mx = v > mx ? v : mx;
+    }
+    if (lane_id() == 0 && mx) atomicMax(rowmax, mx);
+}
+
 // Tile boundaries in merge space, all searched in parallel up front (a
 // dependent ~log2(n)-step binary search per CTA would otherwise sit on the
 // critical path of every tile).
 __global__ void k_spmv_partition(const uint32_t* __restrict__ offsets, uint32_t n, uint64_t m, uint64_t tiles,
-                                 uint32_t* coords) {
+                                 const uint32_t* __restrict__ rowmax, uint32_t* coords) {
     const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b > tiles) return;
     const uint64_t total = (uint64_t)n + m;
     const uint64_t d = b * kSpTile < total ? b * kSpTile : total;
-    coords[b] = (uint32_t)merge_search(offsets + 1, n, 0, m, d);
+    coords[b] = (uint32_t)merge_search(offsets + 1, n, 0, m, d) | (*rowmax <= kSpRowMax ? kSpRowMode : 0u);
+}
+
+template <typename T>
+__device__ __forceinline__ T row_sum(const uint32_t* __restrict__ indices, const T* __restrict__ w,
+                                     const T* __restrict__ x, uint32_t b, uint32_t len) {
+    T acc = 0;
+#pragma unroll
+    for (uint32_t j0 = 0; j0 < kSpRowMax; j0 += 4) {
+        if (j0 >= len) break;
+        uint32_t c[4];
+#pragma unroll
+        for (uint32_t j = 0; j < 4; j++) c[j] = j0 + j < len ? __ldg(indices + b + j0 + j) : 0u;
+        T v[4];
+#pragma unroll
+        for (uint32_t j = 0; j < 4; j++) v[j] = j0 + j < len ? __ldg(x + c[j]) : T(0);
+#pragma unroll
+        for (uint32_t j = 0; j < 4; j++)
+            if (j0 + j < len) acc += w ? v[j] * __ldg(w + b + j0 + j) : v[j];
+    }
+    return acc;
+}
+
+// Row mode: one thread per row (grid-stride over the rows), its indices and
+// gathers in flight four at a time -- the kernel stays at 32 registers, 16
+// CTAs/SM, which the merge path needs (two rows per thread: 40 registers).
+template <typename T>
+__device__ __forceinline__ void spmv_rows(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ indices,
+                                          const T* __restrict__ w, const T* __restrict__ x, T* __restrict__ y,
+                                          uint32_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * kSpNT;
+    for (uint64_t r = (uint64_t)blockIdx.x * kSpNT + threadIdx.x; r < n; r += stride) {
+        const uint32_t b = __ldg(offsets + r);
+        y[r] = row_sum<T>(indices, w, x, b, __ldg(offsets + r + 1) - b);
+    }
 }
 
 // Merge-path search inside a tile, all tile-relative 32-bit: a[] holds the
@@ -111,14 +177,14 @@ template <typename T, bool VEC>
 __device__ __forceinline__ void spmv_tile(uint64_t tile, const uint32_t* __restrict__ offsets,
                                           const uint32_t* __restrict__ indices, const T* __restrict__ w,
                                           const T* __restrict__ x, T* __restrict__ y, uint32_t n, uint64_t m,
-                                          const uint32_t* __restrict__ coords, uint32_t* __restrict__ tile_head,
+                                          uint32_t c_lo, uint32_t c_hi, uint32_t* __restrict__ tile_head,
                                           T* __restrict__ tile_tail, uint32_t* s_end, T* s_val, SegValT<T>* s_warp) {
     using SegVal = SegValT<T>;
     const uint32_t gt = threadIdx.x;
     const uint64_t total = (uint64_t)n + m;
     const uint64_t d0 = tile * kSpTile;
     const uint32_t items_tile = (uint32_t)((d0 + kSpTile < total ? d0 + kSpTile : total) - d0);
-    const uint32_t i0 = __ldg(coords + tile), i1 = __ldg(coords + tile + 1);
+    const uint32_t i0 = c_lo & ~kSpRowMode, i1 = c_hi & ~kSpRowMode;
     const uint64_t j0 = d0 - i0;
     // A reused partition (reuse_partition = 1) that does not belong to this
     // CSR could hold any coords: never index s_end / s_val past the tile.
@@ -310,10 +376,19 @@ __global__ void __launch_bounds__(kSpNT) k_spmv_merge(const uint32_t* __restrict
                                                       uint32_t* __restrict__ tile_head, T* __restrict__ tile_tail,
                                                       const int* stop) {
     if (stop && *(volatile const int*)stop) return;
+    // The mode rides in bit 31 of the tile's own coordinate, so merge mode
+    // waits on no extra load (measured: a separate mode word, or coords[0],
+    // costs the R-MAT SpMV 1-2 %).
+    const uint32_t c_lo = __ldg(coords + blockIdx.x), c_hi = __ldg(coords + blockIdx.x + 1);
+    if (c_lo & kSpRowMode) {
+        spmv_rows<T>(offsets, indices, w, x, y, n);
+        return;
+    }
     __shared__ uint32_t s_end[kSpTile + 1];
     __shared__ __align__(16) T s_val[kSpTile + 4];
     __shared__ SegValT<T> s_warp[kSpNT / 32];
-    spmv_tile<T, VEC>(blockIdx.x, offsets, indices, w, x, y, n, m, coords, tile_head, tile_tail, s_end, s_val, s_warp);
+    spmv_tile<T, VEC>(blockIdx.x, offsets, indices, w, x, y, n, m, c_lo, c_hi, tile_head, tile_tail, s_end, s_val,
+                      s_warp);
 }
 
 // Chunk aggregates of the per-CTA (has_head, tail) pairs: a segmented sum
@@ -365,8 +440,9 @@ __device__ __forceinline__ SegValT<T> block_seg_scan(SegValT<T> v, SegValT<T>* s
 template <typename T>
 __global__ void __launch_bounds__(kSpChunk) k_spmv_chunk_agg(const uint32_t* __restrict__ tile_head,
                                                              const T* __restrict__ tile_tail, uint64_t tiles,
-                                                             unsigned* chunk_flag, T* chunk_val, const int* stop) {
-    if (stop && *(volatile const int*)stop) return;
+                                                             unsigned* chunk_flag, T* chunk_val,
+                                                             const uint32_t* __restrict__ coords, const int* stop) {
+    if ((stop && *(volatile const int*)stop) || (__ldg(coords) & kSpRowMode)) return;
     using SegVal = SegValT<T>;
     __shared__ SegVal s_w[33];
     const uint64_t t = (uint64_t)blockIdx.x * kSpChunk + threadIdx.x;
@@ -386,8 +462,9 @@ template <typename T>
 __global__ void __launch_bounds__(kSpChunk) k_spmv_carry(const uint32_t* __restrict__ tile_head,
                                                          const T* __restrict__ tile_tail, uint64_t tiles,
                                                          const unsigned* __restrict__ chunk_flag,
-                                                         const T* __restrict__ chunk_val, T* y, const int* stop) {
-    if (stop && *(volatile const int*)stop) return;
+                                                         const T* __restrict__ chunk_val, T* y,
+                                                         const uint32_t* __restrict__ coords, const int* stop) {
+    if ((stop && *(volatile const int*)stop) || (__ldg(coords) & kSpRowMode)) return;
     using SegVal = SegValT<T>;
     __shared__ SegVal s_w[33];
     __shared__ T s_cin;
@@ -416,7 +493,7 @@ size_t spmv_workspace_bytes(uint32_t n, uint64_t m) {
     const uint64_t tiles = ceil_div((uint64_t)n + m, kSpTile);
     const uint64_t chunks = ceil_div(tiles, kSpChunk);
     const size_t arr = ((tiles + 2) * 8 + 255) / 256 * 256;   // sized for double
-    return arr * 3 + ((chunks + 1) * 16 + 255) / 256 * 256;
+    return arr * 3 + ((chunks + 1) * 16 + 255) / 256 * 256 + 256;  // + rowmax
 }
 
 template <typename T>
@@ -434,8 +511,13 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
     T* tile_tail = reinterpret_cast<T*>(p + 2 * arr);
     unsigned* chunk_flag = reinterpret_cast<unsigned*>(p + 3 * arr);
     T* chunk_val = reinterpret_cast<T*>(p + 3 * arr + ((chunks + 1) * 4 + 15) / 16 * 16);
-    if (!partitioned)  // coords depend on the structure only: iterative callers compute them once
-        k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, coords);
+    uint32_t* rowmax = reinterpret_cast<uint32_t*>(p + 3 * arr + ((chunks + 1) * 16 + 255) / 256 * 256);
+    if (!partitioned) {  // coords and the longest row depend on the structure only: computed once
+        if (cudaError_t e = cudaMemsetAsync(rowmax, 0, 4, s)) return e;
+        const uint64_t blocks = ceil_div(n, 256), cap = 2048;
+        k_spmv_rowmax<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(offsets, n, rowmax);
+        k_spmv_partition<<<(unsigned)ceil_div(tiles + 1, 256), 256, 0, s>>>(offsets, n, m, tiles, rowmax, coords);
+    }
     // (A persistent variant with a 128 KB shared-memory copy of the hub prefix of x
     // was measured slower at c2/c3: the occupancy it costs outweighs the hits.)
     const bool vec = !w && (reinterpret_cast<uintptr_t>(indices) & 15) == 0;
@@ -452,16 +534,16 @@ cudaError_t launch_spmv_t(const uint32_t* offsets, const uint32_t* indices, cons
                       sizeof(T) == 4 ? 50 : 66);
     }
     if (vec)
-        k_spmv_merge<T, true><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords,
-                                                                          tile_head, tile_tail, stop);
+        k_spmv_merge<T, true><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head,
+                                                               tile_tail, stop);
     else
         k_spmv_merge<T, false><<<(unsigned)tiles, kSpNT, 0, s>>>(offsets, indices, w, x, y, n, m, coords, tile_head,
-                                                                 tile_tail, stop);
+                                                                tile_tail, stop);
     if (tiles > 1) {
         k_spmv_chunk_agg<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val,
-                                                                 stop);
+                                                                 coords, stop);
         k_spmv_carry<T><<<(unsigned)chunks, kSpChunk, 0, s>>>(tile_head, tile_tail, tiles, chunk_flag, chunk_val, y,
-                                                             stop);
+                                                             coords, stop);
     }
     return cudaGetLastError();
 }

@@ -326,6 +326,68 @@ def test_spmv_vector_staging_edges(dev, n, mod, dtype):
     assert np.array_equal(y_vec.cpu().numpy().astype(np.float64), want)
 
 
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("maxdeg", [8, 9])
+@pytest.mark.parametrize("n", [1, 129, 70001])
+def test_spmv_row_mode_switch(dev, n, maxdeg, dtype):
+    """Row mode (no row longer than 8: one thread per row) and merge mode
+    (a row of 9) on otherwise equal matrices: each equals the oracle exactly on
+    integer data, weighted and not, fp32 and fp64; a workspace partitioned for
+    one mode and re-partitioned for the other follows the new matrix (the
+    mode is decided at partition time), and back."""
+    import torch
+
+    rng = np.random.default_rng(n * 10 + maxdeg)
+    deg = rng.choice([0, 1, 2, 3, 4, 5, 8], size=n)
+    deg[n // 2] = maxdeg
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(deg)
+    m = int(off[-1])
+    idx = rng.integers(0, n, m)
+    x = rng.integers(0, 4, n).astype(dtype)
+    wt = rng.integers(1, 3, m).astype(dtype)
+    t = lambda a: torch.from_numpy(a.astype(np.uint32).view(np.int32)).cuda()  # noqa: E731
+    t_off, t_idx, xs, ws_ = t(off), t(idx), torch.from_numpy(x).cuda(), torch.from_numpy(wt).cuda()
+    want = oracle.spmv_pull(off, idx, x.astype(np.float64))
+    want_w = oracle.spmv_pull(off, idx, x.astype(np.float64), wt.astype(np.float64))
+    ws = dev.spmv_workspace(n, m, "cuda")
+    y = dev.spmv(t_off, t_idx, xs, ws=ws)
+    assert np.array_equal(y.cpu().numpy().astype(np.float64), want)
+    yw = dev.spmv(t_off, t_idx, xs, weights=ws_, ws=ws, reuse_partition=True)
+    assert np.array_equal(yw.cpu().numpy().astype(np.float64), want_w)
+    # the other mode on the same workspace: one row grows past / shrinks to the bound
+    deg2 = deg.copy()
+    deg2[n // 2] = 17 - maxdeg
+    off2 = np.zeros(n + 1, np.int64)
+    off2[1:] = np.cumsum(deg2)
+    idx2 = rng.integers(0, n, int(off2[-1]))
+    y2 = dev.spmv(t(off2), t(idx2), xs, ws=ws)
+    assert np.array_equal(y2.cpu().numpy().astype(np.float64), oracle.spmv_pull(off2, idx2, x.astype(np.float64)))
+    y3 = dev.spmv(t_off, t_idx, xs, ws=ws)
+    assert torch.equal(y3, y)
+
+
+def test_spmv_row_mode_grid_float_and_pagerank(bb, dev):
+    """The c3-shaped case (a grid: every row <= 4, row mode) with random x:
+    fp32 within the north star's 1e-5 of the oracle's fp64 sums, bitwise
+    repeatable; PageRank (fp64 SpMV iterations with the device stop flag) on
+    the grid matches the oracle."""
+    import torch
+
+    I, J = dev.generate_grid(300, 257)
+    n = 300 * 257
+    off, idx, _ = dev.coo_to_csr(I, J, n)
+    x = torch.rand(n, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))
+    y = dev.spmv(off, idx, x)
+    want = oracle.spmv_pull(to_np(off), to_np(idx), x.cpu().numpy().astype(np.float64))
+    np.testing.assert_allclose(y.cpu().numpy(), want, rtol=1e-5, atol=0)
+    assert torch.equal(y, dev.spmv(off, idx, x))
+    pr, it = dev.pagerank(off, idx)
+    ex, eit = oracle.pagerank(to_np(off), to_np(idx), n)
+    assert int(it.cpu()[0]) == eit
+    np.testing.assert_allclose(pr.cpu().numpy(), ex, rtol=PR_RTOL, atol=1e-15)
+
+
 def test_host_pipeline_matches_device(dev):
     import torch
 
