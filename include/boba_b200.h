@@ -249,6 +249,11 @@ int boba_widen_ids(const uint32_t *in, uint64_t count, int64_t *out, void *strea
 int boba_host_to_device_ids(const int64_t *host, uint64_t count, uint64_t bound, uint32_t *dev,
                             int64_t *bad_index, void *stream);
 int boba_device_to_host_ids(const uint32_t *dev, uint64_t count, int64_t *host, void *stream);
+/* boba_device_to_host_ids for a first-occurrence array: 0xFFFFFFFF (never
+ * seen) widens to INT64_MAX, the reference's RANK_UNSET (_parallel.py:31), in
+ * the same pass (replaces the numpy fix-up of `boba_parallel(...,
+ * return_ranks=True)`'s rank array, ordering.py:99-151). */
+int boba_device_to_host_ranks(const uint32_t *dev, uint64_t count, int64_t *host, void *stream);
 /* offsets[0..n] = exclusive prefix sum of counts[0..n) (offsets[n] = total):
  * np.cumsum of graph.py:270-272 on the device. */
 size_t boba_exclusive_scan_workspace_size(uint64_t count);

@@ -91,6 +91,7 @@ SIGNATURES = {
     "boba_narrow_ids": ([_P, _U64, _U64, _P, ctypes.POINTER(ctypes.c_int64), _P], _I),
     "boba_host_to_device_ids": ([_P, _U64, _U64, _P, ctypes.POINTER(ctypes.c_int64), _P], _I),
     "boba_device_to_host_ids": ([_P, _U64, _P, _P], _I),
+    "boba_device_to_host_ranks": ([_P, _U64, _P, _P], _I),
     "boba_widen_ids": ([_P, _U64, _P, _P], _I),
     "boba_exclusive_scan_workspace_size": ([_U64], _SZ),
     "boba_exclusive_scan_u32": ([_P, _U32, _P, _P, _SZ, _P], _I),

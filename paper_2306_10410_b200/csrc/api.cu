@@ -598,6 +598,11 @@ int boba_device_to_host_ids(const uint32_t* dev, uint64_t count, int64_t* host, 
     return cuda_status(boba::host_d2h_ids(dev, count, host, S(stream)), "boba_device_to_host_ids");
 }
 
+int boba_device_to_host_ranks(const uint32_t* dev, uint64_t count, int64_t* host, void* stream) {
+    REQUIRE((host && dev) || count == 0, "boba_device_to_host_ranks: NULL argument");
+    return cuda_status(boba::host_d2h_ids(dev, count, host, S(stream), true), "boba_device_to_host_ranks");
+}
+
 int boba_widen_ids(const uint32_t* in, uint64_t count, int64_t* out, void* stream) {
     REQUIRE((in && out) || count == 0, "boba_widen_ids: NULL argument");
     return cuda_status(boba::launch_widen(in, count, out, num_sms(), S(stream)), "boba_widen_ids");

@@ -122,7 +122,8 @@ cudaError_t host_h2d_ids(const int64_t* host, uint64_t count, uint64_t bound, ui
     return cudaSuccess;
 }
 
-cudaError_t host_d2h_ids(const uint32_t* dev, uint64_t count, int64_t* host, cudaStream_t s) {
+// unset_to_max: 0xFFFFFFFF widens to INT64_MAX (the reference's RANK_UNSET)
+cudaError_t host_d2h_ids(const uint32_t* dev, uint64_t count, int64_t* host, cudaStream_t s, bool unset_to_max) {
     if (count == 0) return cudaSuccess;
     Staging* st = nullptr;
     cudaError_t e = staging_for_device(st);
@@ -144,7 +145,10 @@ cudaError_t host_d2h_ids(const uint32_t* dev, uint64_t count, int64_t* host, cud
         const uint32_t* buf = st->slot[k & 1];
         parallel_for(len, [&](size_t lo, size_t hi) {
             int64_t* dst = host + c0;
-            for (size_t i = lo; i < hi; i++) dst[i] = (int64_t)buf[i];
+            if (unset_to_max)
+                for (size_t i = lo; i < hi; i++) dst[i] = buf[i] == 0xFFFFFFFFu ? INT64_MAX : (int64_t)buf[i];
+            else
+                for (size_t i = lo; i < hi; i++) dst[i] = (int64_t)buf[i];
         });
     }
     return cudaSuccess;

@@ -126,6 +126,6 @@ cudaError_t launch_row_cut(const uint32_t* hist_g, const uint32_t* hist_l, uint3
 // host <-> device id transfers through pinned staging (hostio.cu); synchronous
 cudaError_t host_h2d_ids(const int64_t* host, uint64_t count, uint64_t bound, uint32_t* dev, int64_t* bad,
                          cudaStream_t s);
-cudaError_t host_d2h_ids(const uint32_t* dev, uint64_t count, int64_t* host, cudaStream_t s);
+cudaError_t host_d2h_ids(const uint32_t* dev, uint64_t count, int64_t* host, cudaStream_t s, bool unset_to_max = false);
 
 }  // namespace boba

@@ -45,7 +45,7 @@ def boba_parallel(g, mode: str = "deterministic", thread_hint: int | None = None
     if mode not in _MODES:
         raise ValueError(f"unknown mode: {mode!r}")
     relaxed = mode == "relaxed" and thread_hint is not None and int(thread_hint) > 1
-    r, order, label, dlabel = _host.boba(g.I, g.J, int(g.n), relaxed=relaxed)
+    r, order, label, dlabel = _host.boba(g.I, g.J, int(g.n), relaxed=relaxed, ranks=return_ranks)
     p = Permutation(order, label)
     if dlabel is not None:   # apply_permutation(g, p) reuses the device label
         _host.remember(p.label, dlabel)
