@@ -106,10 +106,31 @@ __device__ __forceinline__ uint32_t rank_of(uint32_t f, const uint4* __restrict_
     return rank;
 }
 
+// Rank of position f from its record (lo = words 0-3, hi = words 4-6 + the
+// record's prefix), branch-free.
+__device__ __forceinline__ uint32_t rank_in_record(const uint4& lo, const uint4& hi, uint32_t f) {
+    const uint32_t w = f >> 5, wi = w - rec_of_word(w) * kRecWords, below = (1u << (f & 31)) - 1u;
+    const uint32_t words[kRecWords] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z};
+    uint32_t rank = hi.w;
+#pragma unroll
+    for (int k = 0; k < kRecWords; k++)
+        rank += __popc(words[k] & ((uint32_t)k < wi ? 0xFFFFFFFFu : ((uint32_t)k == wi ? below : 0u)));
+    return rank;
+}
+
+// Record loads in flight per thread: the lookups are independent DRAM
+// round trips (the record array is beyond L2 at s26), so they are issued in
+// batches rather than one vertex at a time (measured, P2 c4 / c5 / c2: one
+// at a time 2.69 / 0.392 / 0.111 ms, batches of 2 2.61 / 0.371 / 0.101,
+// 4: 2.62 / 0.370 / 0.101, all 8: 2.58 / 0.350 / 0.097).
+#ifndef ASSIGN_BATCH
+#define ASSIGN_BATCH 8
+#endif
+
 __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__ first, uint32_t n,
                                                     const uint4* __restrict__ recs,
                                                     const uint32_t* __restrict__ n_seen_ptr,
-                                                    uint32_t* order, uint32_t* label,
+                                                    uint32_t* __restrict__ order, uint32_t* __restrict__ label,
                                                     unsigned long long* status, unsigned* tile_counter) {
     __shared__ unsigned s_tile;
     __shared__ uint32_t s_scan[kScanNT / 32 + 1];
@@ -126,10 +147,35 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
         iso += (v0 + k < n && f[k] == BOBA_UNSET);
     }
     uint32_t total;
-    uint32_t iso_excl = block_exclusive_sum<kScanNT>(iso, s_scan, &total);
+    const uint32_t iso_excl = block_exclusive_sum<kScanNT>(iso, s_scan, &total);
+    // publish the tile's aggregate now; the lookback comes after the rank
+    // lookups, so its wait overlaps them
+    if (threadIdx.x == 0)
+        st_volatile_u64(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | (unsigned long long)total);
+    // seen vertices: rank = record prefix + popcount below the position
+    uint32_t lab[kAssignVPT];
+#pragma unroll
+    for (int k0 = 0; k0 < kAssignVPT; k0 += ASSIGN_BATCH) {
+        uint4 lo[ASSIGN_BATCH], hi[ASSIGN_BATCH];
+#pragma unroll
+        for (int j = 0; j < ASSIGN_BATCH; j++) {
+            const int k = k0 + j;
+            if (v0 + k < n && f[k] != BOBA_UNSET) {
+                const uint32_t r = rec_of_word(f[k] >> 5);
+                lo[j] = __ldg(recs + 2 * r);
+                hi[j] = __ldg(recs + 2 * r + 1);
+            } else {
+                lo[j] = hi[j] = make_uint4(0, 0, 0, 0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < ASSIGN_BATCH; j++) {
+            const int k = k0 + j;
+            lab[k] = rank_in_record(lo[j], hi[j], f[k]);
+            if (v0 + k < n && f[k] != BOBA_UNSET) order[lab[k]] = (uint32_t)(v0 + k);
+        }
+    }
     if (threadIdx.x < 32) {
-        if (threadIdx.x == 0)
-            st_volatile_u64(status + tile, (tile == 0 ? kFlagInc : kFlagAgg) | (unsigned long long)total);
         unsigned long long ex = tile == 0 ? 0ull : warp_lookback(status, (long long)tile);
         if (threadIdx.x == 0) {
             if (tile != 0) st_volatile_u64(status + tile, kFlagInc | (ex + total));
@@ -137,14 +183,14 @@ __global__ void __launch_bounds__(kScanNT) k_assign(const uint32_t* __restrict__
         }
     }
     __syncthreads();
+    // never-seen vertices: n_seen + their ascending rank among them
     uint32_t iso_rank = __ldg(n_seen_ptr) + (uint32_t)s_excl + iso_excl;
-    uint32_t lab[kAssignVPT];
 #pragma unroll
     for (int k = 0; k < kAssignVPT; k++) {
-        if (v0 + k >= n) continue;
-        uint32_t r = (f[k] == BOBA_UNSET) ? iso_rank++ : rank_of(f[k], recs);
-        lab[k] = r;
-        order[r] = (uint32_t)(v0 + k);
+        if (v0 + k < n && f[k] == BOBA_UNSET) {
+            lab[k] = iso_rank++;
+            order[lab[k]] = (uint32_t)(v0 + k);
+        }
     }
     if (v0 + kAssignVPT <= n && (reinterpret_cast<uintptr_t>(label) & 15) == 0) {
 #pragma unroll
