@@ -1,3 +1,6 @@
+#!/bin/sh
+# A/B of the rank-assignment batch size (needs: sh tools/build_variant.sh base "" built from the one-at-a-time
+# source, b8 "-DASSIGN_BATCH=8", b2 "-DASSIGN_BATCH=2"); the in-tree build is batch 4 at the time of the run.
 cd $GRAFT_REPO_ROOT 2>/dev/null || cd /root/repo
 for r in 1 2; do
  for L in ab/base/pkg/libboba_b200.so paper_2306_10410_b200/libboba_b200.so ab/b8/pkg/libboba_b200.so ab/b2/pkg/libboba_b200.so; do
