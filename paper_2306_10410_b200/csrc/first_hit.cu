@@ -142,9 +142,12 @@ __device__ __forceinline__ bool seen_swar(const uint32_t* set, const HubHash& hh
     return (z & kHigh) != 0 && tag != kTagMask;        // all-ones tags are never inserted (empty marker)
 }
 
+#ifndef FH_PROBE_CACHE
+#define FH_PROBE_CACHE "cg"
+#endif
 __device__ __forceinline__ uint32_t ld_cg_pred(const uint32_t* p, bool pred) {
     uint32_t r = 0;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cg.u32 %0, [%1];\n\t}"
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global." FH_PROBE_CACHE ".u32 %0, [%1];\n\t}"
                  : "+r"(r)
                  : "l"(p), "r"((uint32_t)pred));
     return r;
