@@ -334,17 +334,20 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
     __syncthreads();
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
+    auto stage = [&](int i) {
+        const uint32_t r = rank[i] + wh[(i / (IPT / C::SUB)) * B + op(key[i])];
+        s_kv[kv_swz(r)] = make_uint2(key[i], vals_in ? wraw[i * 32 + lane] : (uint32_t)(wslot + (uint64_t)i * 32 + lane));
+    };
+    if (full) {
 #pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        if (rank[i] != 0xFFFFFFFFu) {
-            const uint32_t r = rank[i] + wh[(i / (IPT / C::SUB)) * B + op(key[i])];
-            s_kv[kv_swz(r)] = make_uint2(key[i], vals_in ? wraw[i * 32 + lane] : (uint32_t)(wslot + (uint64_t)i * 32 + lane));
-        }
+        for (int i = 0; i < IPT; i++) stage(i);
+    } else {
+#pragma unroll
+        for (int i = 0; i < IPT; i++)
+            if (rank[i] != 0xFFFFFFFFu) stage(i);
     }
     __syncthreads();
-    const uint64_t rem = m - tile_base;
-    const int items = rem < (uint64_t)TILE ? (int)rem : TILE;
-    for (int j = threadIdx.x; j < items; j += NT) {
+    auto emit = [&](int j) {
         const uint2 kv = s_kv[kv_swz(j)];
         const uint32_t d = op(kv.x);
         const uint32_t g = s_glob[d] + (uint32_t)j;
@@ -361,6 +364,14 @@ __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __
             else if (s_kv[kv_swz(j - 1)].x != kv.x)
                 row_starts[kv.x] = g;
         }
+    };
+    // full tiles: a fixed trip count, unrolled (no per-item bound or rank-valid checks)
+    if (full) {
+#pragma unroll
+        for (int k = 0; k < IPT; k++) emit((int)threadIdx.x + k * NT);
+    } else {
+        const int items = (int)(m - tile_base);
+        for (int j = threadIdx.x; j < items; j += NT) emit(j);
     }
 }
 
