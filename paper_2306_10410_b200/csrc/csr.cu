@@ -443,7 +443,7 @@ cudaError_t launch_sort_pairs(const uint32_t* keys, const uint32_t* vals, uint64
         const bool last = i == passes - 1;
         uint32_t* kout = last ? keys_out : W.bufs[(i & 1) * 2];
         uint32_t* vout = last ? vals_out : W.bufs[(i & 1) * 2 + 1];
-        cudaError_t e = radix_pass<8, 256, 16, 4>(kin, vin, count, sh, bits, W.H, W.st, W.counter, kout, vout,
+        cudaError_t e = radix_pass<8, 256, 16, RADIX_MINB>(kin, vin, count, sh, bits, W.H, W.st, W.counter, kout, vout,
                                                   num_sms, s, nullptr);
         if (e != cudaSuccess) return e;
         kin = kout;
@@ -490,7 +490,7 @@ cudaError_t launch_range_partition(const uint32_t* keys, const uint32_t* vals, u
     uint32_t* H = reinterpret_cast<uint32_t*>(p);
     unsigned long long* st = reinterpret_cast<unsigned long long*>(p + (hcount * 4 + 255) / 256 * 256);
     unsigned* counter = reinterpret_cast<unsigned*>(st + ceil_div(hcount, kScanTile) + 1);
-    cudaError_t e = radix_pass_op<8, 256, 16, 4, DigitRange>(keys, vals, m, DigitRange{bounds, parts, relative}, bits, H, st,
+    cudaError_t e = radix_pass_op<8, 256, 16, RADIX_MINB, DigitRange>(keys, vals, m, DigitRange{bounds, parts, relative}, bits, H, st,
                                                              counter, keys_out, vals_out, num_sms, s);
     if (e != cudaSuccess) return e;
     if (counts_out) k_part_counts<<<1, 256, 0, s>>>(H, tiles, parts, m, counts_out);
@@ -574,7 +574,7 @@ cudaError_t launch_coo_to_csr(const uint32_t* I2, const uint32_t* J2, const doub
             // pass i writes bufs[2(i&1)], bufs[2(i&1)+1]; it reads the other parity.
             uint32_t* kout = last ? nullptr : W.bufs[(i & 1) * 2];
             uint32_t* vout = (last && !weighted) ? indices : W.bufs[(i & 1) * 2 + 1];
-            cudaError_t r = radix_pass<8, 256, 16, 4>(ki, vi, m, q.shift[i], q.bits[i], W.H, W.scan_status,
+            cudaError_t r = radix_pass<8, 256, 16, RADIX_MINB>(ki, vi, m, q.shift[i], q.bits[i], W.H, W.scan_status,
                                                       W.counters, kout, vout, num_sms, st,
                                                       (last && !counts_in) ? offsets : nullptr,
                                                       i == 0 && first_hist_ready, in_body);

@@ -25,6 +25,10 @@
 #ifndef RADIX_SUB
 #define RADIX_SUB 1
 #endif
+// resident downsweep CTAs per SM the register allocation is bounded for
+#ifndef RADIX_MINB
+#define RADIX_MINB 4
+#endif
 
 namespace boba {
 
@@ -208,7 +212,11 @@ __device__ __forceinline__ void rank_slots(const uint32_t (&key)[IPT], uint32_t 
 // multiple of 16 entries -- 16 x 8 B = one full bank cycle -- and all land in
 // one bank pair; XOR-ing the low 4 bits with the next 4 spreads them (a
 // bijection on every aligned group of 256 slots).
+#ifndef RADIX_NO_SWZ
 __device__ __forceinline__ uint32_t kv_swz(uint32_t r) { return r ^ ((r >> 4) & 15u); }
+#else
+__device__ __forceinline__ uint32_t kv_swz(uint32_t r) { return r; }
+#endif
 
 template <int RB, int NT, int IPT, int MINB, typename Op>
 __global__ void __launch_bounds__(NT, MINB) k_radix_downsweep(const uint32_t* __restrict__ keys_in,
