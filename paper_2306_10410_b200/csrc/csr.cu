@@ -109,7 +109,10 @@ __global__ void k_row_starts(const uint32_t* __restrict__ keys, uint64_t m, uint
     if (blockIdx.x == 0 && threadIdx.x == 0) offsets[n] = (uint32_t)m;
 }
 
-constexpr int kSmNT = 256, kSmIPT = 16, kSmTile = kSmNT * kSmIPT;
+#ifndef SCAN_IPT
+#define SCAN_IPT 64
+#endif
+constexpr int kSmNT = 256, kSmIPT = SCAN_IPT, kSmTile = kSmNT * kSmIPT;
 
 // In-place suffix minimum over data[0..count).  Tiles are aligned to
 // multiples of kSmTile from the bottom and taken from the top (tile k of T
