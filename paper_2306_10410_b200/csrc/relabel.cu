@@ -135,7 +135,10 @@ __global__ void __launch_bounds__(kRlNT, 1) k_relabel_range(const uint4* __restr
                                                             uint32_t lo, uint32_t width, uint4* I2, uint4* J2,
                                                             RowTileHist rh) {
     // HIST: TPI tiles per iteration, so the barrier comes once per 16K edges
-    constexpr int TPI = HIST ? 4 : 1;
+#ifndef RL_TPI
+#define RL_TPI 1
+#endif
+    constexpr int TPI = HIST ? 4 : RL_TPI;
     __shared__ uint32_t s_h[2][TPI][HIST ? kRlHistMax : 1];
     if (HIST) {
         for (int i = threadIdx.x; i < 2 * TPI * kRlHistMax; i += kRlNT) (&s_h[0][0][0])[i] = 0;
