@@ -28,7 +28,10 @@ namespace boba {
 constexpr int kScanNT = 256;
 constexpr int kRecWords = 7;                            // bitmap words per 32-byte record
 constexpr uint32_t kRecBits = 32 * kRecWords;           // 224 positions per record
-constexpr int kRecsPerThread = 4;
+#ifndef RECS_PER_THREAD
+#define RECS_PER_THREAD 4
+#endif
+constexpr int kRecsPerThread = RECS_PER_THREAD;
 constexpr int kRecsPerTile = kScanNT * kRecsPerThread;
 // vertices per thread (multiple of 4; measured c4 / c5 P2: 4 -> 2.71 / 0.41 ms,
 // 8 -> 2.69 / 0.39, 16 -> 2.74 / 0.41)
