@@ -112,7 +112,10 @@ __global__ void k_row_starts(const uint32_t* __restrict__ keys, uint64_t m, uint
 #ifndef SCAN_IPT
 #define SCAN_IPT 64
 #endif
-constexpr int kSmNT = 256, kSmIPT = SCAN_IPT, kSmTile = kSmNT * kSmIPT;
+#ifndef SMIN_IPT
+#define SMIN_IPT SCAN_IPT
+#endif
+constexpr int kSmNT = 256, kSmIPT = SMIN_IPT, kSmTile = kSmNT * kSmIPT;
 
 // In-place suffix minimum over data[0..count).  Tiles are aligned to
 // multiples of kSmTile from the bottom and taken from the top (tile k of T
